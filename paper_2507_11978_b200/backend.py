@@ -1,0 +1,270 @@
+"""The drop-in B200 executor: ``launch`` (twin of the reference's
+``sim.launch``) and the per-kernel ``{name}_launch`` launchers (twins of the
+emitted Triton launchers).
+
+Reference contracts mirrored here:
+
+* ``launch(checked, args, meta)`` - sim.py:163-236.  Same argument
+  validation and ``LaunchError`` conditions (missing / non-positive /
+  unexpected meta, missing / unexpected argument, wrong rank,
+  sim.py:128-150), same launch-time checks (sim.py:153-160) and grid
+  evaluation (sim.py:176-183, "grid dimension evaluated to g").  ``args``
+  maps parameter names to CUDA ``torch.Tensor``s (strides in elements, as
+  ``ConcreteTensor.strides``) and rank-0 parameters to Python floats.
+  Returns ``LaunchResult(grid, total)``.
+* ``{name}_launch(*params, *meta)`` - emit.py:267-293: positional
+  parameters in KernelSpec order, then meta; reads ``.shape``/``.stride()``,
+  asserts the checks, launches, returns the out-parameters.
+
+Execution: the CheckedSpec's maps are compiled to the native map VM
+(bytecode.py) which evaluates checks and grid; the spec is matched to a
+kernel family by name AND by structural identity of its grid, checks,
+index maps and application IR with this package's catalog (so a spec built
+by the reference front end is accepted only if it computes what the native
+kernel computes); then ``ntb_launch`` runs the hand-written sm_100a kernel.
+Unmatched specs raise ``UnsupportedSpecError``; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+from typing import Mapping
+
+import numpy as np
+
+from . import _lib
+from . import symbolic as se
+from .bytecode import MapProgram, build_program
+from .catalog import ALL_NAMES, checked as canonical
+from .spec import ir_tree
+
+
+class LaunchError(Exception):
+    """Bad launch configuration (reference sim.LaunchError, sim.py:39-41)."""
+
+
+class UnsupportedSpecError(LaunchError):
+    """The spec does not match any sm_100a kernel family."""
+
+
+class BackendError(RuntimeError):
+    """CUDA / native-library failure."""
+
+
+@dataclass(frozen=True)
+class LaunchResult:
+    grid: tuple
+    total: int
+
+
+_DTYPES = None
+
+
+def _dtype_code(t):
+    global _DTYPES
+    import torch
+
+    if _DTYPES is None:
+        _DTYPES = {torch.float32: _lib.NTB_F32, torch.float16: _lib.NTB_F16,
+                   torch.bfloat16: _lib.NTB_BF16}
+    try:
+        return _DTYPES[t.dtype]
+    except KeyError:
+        raise LaunchError(f"unsupported element type {t.dtype}") from None
+
+
+# ---- spec -> (family, program) cache --------------------------------------
+
+_cache_lock = threading.Lock()
+_cache: dict = {}
+
+
+def _fingerprint(checked):
+    """Structural identity of a CheckedSpec: grid, checks, maps, IR."""
+    spec = checked.spec
+    maps = []
+    for p in spec.params:
+        if p.rank < 1:
+            continue
+        m = checked.index_maps[p.name]
+        maps.append((
+            p.name,
+            tuple(se.from_any(s).node for s in m.lane_sizes),
+            tuple(se.from_any(s).node for s in m.nest_sizes),
+            se.from_any(m.offset).node,
+            tuple((se.from_any(a).node, se.from_any(b).node) for a, b in m.mask),
+        ))
+    return (
+        spec.name,
+        tuple((p.name, p.rank, p.role) for p in spec.params),
+        tuple(spec.meta),
+        tuple(se.from_any(s).node for s in checked.grid.sizes),
+        tuple((se.from_any(a).node, se.from_any(b).node) for a, b in checked.grid.checks),
+        tuple(maps),
+        repr(ir_tree(spec.application)),
+    )
+
+
+def _resolve(checked) -> tuple:
+    key = id(checked)
+    with _cache_lock:
+        hit = _cache.get(key)
+        if hit is not None and hit[0] is checked:
+            return hit[1], hit[2]
+    name = checked.spec.name
+    if name not in ALL_NAMES:
+        raise UnsupportedSpecError(f"no sm_100a kernel family for spec {name!r}")
+    if _fingerprint(checked) != _fingerprint(canonical(name)):
+        raise UnsupportedSpecError(
+            f"spec {name!r} does not match the canonical {name} arrangement/application; "
+            "the B200 backend only executes specs whose maps it has a native kernel for")
+    prog = build_program(checked)
+    with _cache_lock:
+        _cache[key] = (checked, name, prog)
+    return name, prog
+
+
+# ---- binding and validation (sim.py:120-160) ------------------------------
+
+def _binding(spec, args: Mapping, meta: Mapping) -> dict:
+    binding: dict = {}
+    for name in spec.meta:
+        if name not in meta:
+            raise LaunchError(f"missing meta-parameter {name!r}")
+        v = int(meta[name])
+        if v < 1:
+            raise LaunchError(f"meta-parameter {name!r} must be positive, got {v}")
+        binding[name] = v
+    for extra in sorted(set(meta) - set(spec.meta)):
+        raise LaunchError(f"unexpected meta-parameter {extra!r}")
+    for p in spec.params:
+        if p.name not in args:
+            raise LaunchError(f"missing argument {p.name!r}")
+        t = args[p.name]
+        if p.rank == 0:
+            continue
+        shape = tuple(t.shape)
+        if len(shape) != p.rank:
+            raise LaunchError(f"argument {p.name!r} has rank {len(shape)}, expected {p.rank}")
+        for i, (size, stride) in enumerate(zip(shape, t.stride())):
+            binding[f"{p.name}_size_{i}"] = int(size)
+            binding[f"{p.name}_stride_{i}"] = int(stride)
+    for extra in sorted(set(args) - {p.name for p in spec.params}):
+        raise LaunchError(f"unexpected argument {extra!r}")
+    return binding
+
+
+def _check_failure(prog: MapProgram, binding: dict) -> str:
+    for (lt, rt), (lhs, rhs) in zip(prog.checks_text, prog.grid.checks):
+        lv, rv = se.evaluate(lhs, binding), se.evaluate(rhs, binding)
+        if lv != rv:
+            return f"launch-time check failed: {lt} = {lv} but {rt} = {rv}"
+    return _lib.last_error()
+
+
+def evaluate_grid(checked, binding: dict) -> tuple:
+    """Checks + grid through the native map VM (ntb_grid_eval)."""
+    _, prog = _resolve(checked)
+    rc, grid = _lib.grid_eval(prog.blob, prog.slots(binding))
+    if rc == _lib.NTB_ERR_CHECK:
+        raise LaunchError(_check_failure(prog, binding))
+    if rc == _lib.NTB_ERR_EVAL:
+        raise LaunchError(_lib.last_error())
+    if rc:
+        raise BackendError(_lib.last_error())
+    return grid
+
+
+def launch(checked, args: Mapping, meta: Mapping, *, stream=None) -> LaunchResult:
+    """Execute a CheckedSpec on the current CUDA device (sim.launch twin)."""
+    import torch
+
+    spec = checked.spec
+    binding = _binding(spec, args, meta)
+    family, prog = _resolve(checked)
+    rc, grid = _lib.grid_eval(prog.blob, prog.slots(binding))
+    if rc == _lib.NTB_ERR_CHECK:
+        raise LaunchError(_check_failure(prog, binding))
+    if rc == _lib.NTB_ERR_EVAL:
+        raise LaunchError(_lib.last_error())
+    if rc:
+        raise BackendError(_lib.last_error())
+    total = int(np.prod(grid))
+
+    tensors = [p for p in spec.params if p.rank >= 1]
+    ts = [args[p.name] for p in tensors]
+    for p, t in zip(tensors, ts):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise LaunchError(
+                f"argument {p.name!r} must be a CUDA tensor (the B200 backend has no CPU path)")
+    dt = _dtype_code(ts[0])
+    for p, t in zip(tensors, ts):
+        if _dtype_code(t) != dt:
+            raise LaunchError(f"argument {p.name!r} has dtype {t.dtype}, expected {ts[0].dtype}")
+    scalars = []
+    for p in spec.params:
+        if p.rank == 0:
+            v = args[p.name]
+            scalars.append(float(v.item() if hasattr(v, "item") else v))
+    n = len(ts)
+    ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for t in ts])
+    sizes = np.array([s for t in ts for s in t.shape], dtype=np.int64)
+    strides = np.array([s for t in ts for s in t.stride()], dtype=np.int64)
+    ranks = (ctypes.c_int * n)(*[t.dim() for t in ts])
+    metas = np.array([binding[m] for m in spec.meta], dtype=np.int64)
+    sc = (ctypes.c_double * max(1, len(scalars)))(*scalars)
+    if stream is None:
+        stream = torch.cuda.current_stream(ts[0].device).cuda_stream
+    with torch.cuda.device(ts[0].device):
+        rc = _lib.lib().ntb_launch(
+            _lib.KERNEL_IDS[family], dt, ptrs, n, sc, len(scalars), _lib.i64(sizes),
+            _lib.i64(strides), ranks, _lib.i64(metas), len(metas), ctypes.c_void_p(stream))
+    if rc == _lib.NTB_ERR_UNSUPPORTED:
+        raise UnsupportedSpecError(_lib.last_error())
+    if rc == _lib.NTB_ERR_ARG or rc == _lib.NTB_ERR_CHECK:
+        raise LaunchError(_lib.last_error())
+    if rc:
+        raise BackendError(_lib.last_error())
+    return LaunchResult(grid=tuple(grid), total=total)
+
+
+def launch_count() -> int:
+    """Kernels launched by libntb200 in this process."""
+    return int(_lib.lib().ntb_launch_count())
+
+
+# ---- emitted-launcher twins (emit.py:267-293) ------------------------------
+
+def make_launcher(checked):
+    spec = checked.spec
+    names = [p.name for p in spec.params] + list(spec.meta)
+    outs = [p.name for p in spec.params if p.role == "out"]
+
+    def launcher(*a, **kw):
+        if len(a) + len(kw) != len(names):
+            raise TypeError(f"{spec.name}_launch takes {len(names)} arguments ({', '.join(names)})")
+        bound = dict(zip(names, a))
+        for k, v in kw.items():
+            if k in bound:
+                raise TypeError(f"duplicate argument {k!r}")
+            bound[k] = v
+        args = {p.name: bound[p.name] for p in spec.params}
+        meta = {m: bound[m] for m in spec.meta}
+        launch(checked, args, meta)
+        res = tuple(bound[o] for o in outs)
+        return res[0] if len(res) == 1 else res
+
+    launcher.__name__ = f"{spec.name}_launch"
+    launcher.__doc__ = f"{spec.name}_launch({', '.join(names)}) on the B200 backend"
+    return launcher
+
+
+def __getattr__(attr):
+    # add_launch, mm_launch, ... built on first use
+    if attr.endswith("_launch") and attr[: -len("_launch")] in ALL_NAMES:
+        fn = make_launcher(canonical(attr[: -len("_launch")]))
+        globals()[attr] = fn
+        return fn
+    raise AttributeError(attr)

@@ -1,0 +1,130 @@
+// add / silu: the tile((BLOCK_SIZE,)) elementwise family
+// (reference catalog.py:121-152; emitted add.py.golden / silu.py.golden).
+//
+// Logical program p of the reference grid covers elements [p*B, p*B + B) of
+// every parameter, each load masked against its own size (fill 0) and the
+// store masked against the output size (add.py.golden:26-30).  The union of
+// the logical programs is [0, grid*B), so the whole op is
+//     out[i] = f(in[i] (i < n_in else 0), other[i] (i < n_other else 0))
+// for i < n_out.  BLOCK_SIZE only shapes the logical grid; the physical
+// launch is a grid-stride loop of 128-bit vectors sized to the SM count.
+//
+// HBM roofline: add moves 3 x n x sizeof(T) bytes, silu 2 x n x sizeof(T).
+#include "common.cuh"
+
+namespace ntb {
+
+struct AddOp {
+  static constexpr int kIn = 2;
+  __device__ __forceinline__ float operator()(float a, float b) const { return a + b; }
+};
+struct SiluOp {
+  static constexpr int kIn = 1;
+  __device__ __forceinline__ float operator()(float x, float) const {
+    return x / (1.0f + expf(-x));
+  }
+};
+
+template <typename T, typename Op, int UNROLL>
+__global__ void __launch_bounds__(256) ew_vec_kernel(const T* __restrict__ a,
+                                                     const T* __restrict__ b,
+                                                     T* __restrict__ out, int64_t n_vec) {
+  using P = Pack<T>;
+  Op op;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (UNROLL - 1) * stride < n_vec; i += UNROLL * stride) {
+    P va[UNROLL], vb[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      va[u].raw = ld_stream(a + (i + u * stride) * P::N);
+      if (Op::kIn == 2) vb[u].raw = ld_stream(b + (i + u * stride) * P::N);
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      float fa[P::N], fb[P::N];
+      va[u].to_float(fa);
+      if (Op::kIn == 2) vb[u].to_float(fb);
+#pragma unroll
+      for (int k = 0; k < P::N; ++k) fa[k] = op(fa[k], Op::kIn == 2 ? fb[k] : 0.f);
+      P r;
+      r.from_float(fa);
+      st_stream(out + (i + u * stride) * P::N, r.raw);
+    }
+  }
+  for (; i < n_vec; i += stride) {
+    P va, vb;
+    va.raw = ld_stream(a + i * P::N);
+    float fa[P::N], fb[P::N];
+    va.to_float(fa);
+    if (Op::kIn == 2) {
+      vb.raw = ld_stream(b + i * P::N);
+      vb.to_float(fb);
+    }
+#pragma unroll
+    for (int k = 0; k < P::N; ++k) fa[k] = op(fa[k], Op::kIn == 2 ? fb[k] : 0.f);
+    P r;
+    r.from_float(fa);
+    st_stream(out + i * P::N, r.raw);
+  }
+}
+
+// Generic path: any element strides / mismatched sizes / unaligned bases.
+template <typename T, typename Op>
+__global__ void ew_generic_kernel(const T* a, int64_t na, int64_t sa, const T* b, int64_t nb,
+                                  int64_t sb, T* out, int64_t no, int64_t so) {
+  Op op;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < no;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float x = i < na ? Elem<T>::to_f(a[i * sa]) : 0.f;
+    float y = (Op::kIn == 2 && i < nb) ? Elem<T>::to_f(b[i * sb]) : 0.f;
+    out[i * so] = Elem<T>::from_f(op(x, y));
+  }
+}
+
+template <typename T, typename Op>
+static int run_ew(const LaunchArgs& A) {
+  const int nin = Op::kIn;
+  const T* a = (const T*)A.ptrs[0];
+  const T* b = nin == 2 ? (const T*)A.ptrs[1] : nullptr;
+  T* out = (T*)A.ptrs[nin];
+  int64_t na = A.sizes[A.base[0]], sa = A.strides[A.base[0]];
+  int64_t nb = nin == 2 ? A.sizes[A.base[1]] : 0, sb = nin == 2 ? A.strides[A.base[1]] : 0;
+  int64_t no = A.sizes[A.base[nin]], so = A.strides[A.base[nin]];
+  if (no == 0) return NTB_OK;
+  constexpr int N = Pack<T>::N;
+  bool fast = sa == 1 && so == 1 && na == no && aligned16(a) && aligned16(out) && no % N == 0 &&
+              (nin == 1 || (sb == 1 && nb == no && aligned16(b)));
+  const int sms = sm_count();
+  if (fast) {
+    int64_t n_vec = no / N;
+    constexpr int U = 4;
+    int64_t blocks = cdiv64(n_vec, 256 * U);
+    int64_t cap = (int64_t)sms * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    ew_vec_kernel<T, Op, U><<<(unsigned)blocks, 256, 0, A.stream>>>(a, b, out, n_vec);
+  } else {
+    int64_t blocks = cdiv64(no, 256);
+    if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    ew_generic_kernel<T, Op><<<(unsigned)blocks, 256, 0, A.stream>>>(a, na, sa, b, nb, sb, out,
+                                                                      no, so);
+  }
+  return check_launch("elementwise");
+}
+
+int launch_elementwise(const LaunchArgs& A) {
+  const bool is_add = A.kernel == NTB_K_ADD;
+  if (A.n_ptrs != (is_add ? 3 : 2)) return fail(NTB_ERR_ARG, "elementwise: wrong parameter count");
+  for (int i = 0; i < A.n_ptrs; ++i)
+    if (A.ranks[i] != 1) return fail(NTB_ERR_ARG, "elementwise: parameters must be rank 1");
+  switch (A.dtype) {
+    case NTB_F32: return is_add ? run_ew<float, AddOp>(A) : run_ew<float, SiluOp>(A);
+    case NTB_F16: return is_add ? run_ew<__half, AddOp>(A) : run_ew<__half, SiluOp>(A);
+    case NTB_BF16:
+      return is_add ? run_ew<__nv_bfloat16, AddOp>(A) : run_ew<__nv_bfloat16, SiluOp>(A);
+    default: return fail(NTB_ERR_UNSUPPORTED, "elementwise: unsupported dtype");
+  }
+}
+
+}  // namespace ntb

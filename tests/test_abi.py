@@ -1,0 +1,120 @@
+"""The C-ABI library: loads, exports every declared entry point, and its
+native map VM reproduces the reference's integer maps bit-exactly (no GPU
+needed: the VM runs on the host)."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from helpers import expr_cases, map_cases, maps
+from paper_2507_11978_b200 import _lib, backend
+from paper_2507_11978_b200 import catalog as C
+from paper_2507_11978_b200 import symbolic as S
+from paper_2507_11978_b200.bytecode import build_program, compile_expr
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "ntb200.h"
+
+
+def test_library_exports_every_declared_symbol():
+    declared = set(re.findall(r"^\s*(?:int|const char\*|int64_t)\s+(ntb_\w+)\(",
+                              HEADER.read_text(), re.M))
+    assert declared == set(_lib.EXPORTS)
+    L = _lib.lib()
+    for name in declared:
+        assert hasattr(L, name)
+    assert L.ntb_abi_version() == 1
+
+
+def test_vm_expression_eval_bit_exact():
+    names = ("a", "b", "c", "d")
+    for c in expr_cases():
+        code = compile_expr(S.from_tree(c["expr"]), names.index)
+        rc, v = _lib.expr_eval(code, [c["binding"][n] for n in names])
+        assert rc == 0 and v == c["value"]
+
+
+def test_vm_zero_divisor_is_eval_error():
+    code = compile_expr(S.var("a") // S.var("b"), ("a", "b").index)
+    rc, _ = _lib.expr_eval(code, [1, 0])
+    assert rc == _lib.NTB_ERR_EVAL
+
+
+def test_vm_grid_and_map_points_match_reference():
+    index, arrays = map_cases()
+    for ci, case in enumerate(index):
+        prog = build_program(C.checked(case["kernel"]))
+        slots = prog.slots(case["binding"])
+        rc, grid = _lib.grid_eval(prog.blob, slots)
+        assert rc == 0, _lib.last_error()
+        assert list(grid) == list(arrays[f"c{ci}_grid"])
+        for p in case["params"]:
+            q = prog.params.index(p["name"])
+            rc, offs, mask = _lib.map_enumerate(prog.blob, q, slots)
+            assert rc == 0, _lib.last_error()
+            np.testing.assert_array_equal(offs, arrays[f"c{ci}_{p['name']}_offs"].reshape(-1))
+            np.testing.assert_array_equal(mask, arrays[f"c{ci}_{p['name']}_mask"].reshape(-1))
+
+
+class _Fake:
+    """Shape/stride carrier for host-side validation tests (no data)."""
+
+    def __init__(self, shape):
+        self.shape = tuple(shape)
+        st, acc = [], 1
+        for s in reversed(self.shape):
+            st.append(acc)
+            acc *= s
+        self._st = tuple(reversed(st))
+
+    def stride(self):
+        return self._st
+
+
+def _mm_args():
+    return {"input": _Fake((4, 4)), "other": _Fake((4, 4)), "output": _Fake((4, 4))}
+
+
+MM_META = {"BLOCK_SIZE_M": 2, "BLOCK_SIZE_N": 2, "BLOCK_SIZE_K": 2}
+
+
+@pytest.mark.parametrize("mutate", ["missing_meta", "zero_meta", "extra_meta", "missing_arg",
+                                    "extra_arg", "wrong_rank", "bad_check"])
+def test_launch_validation_raises_launch_error(mutate):
+    """sim.py:128-160 conditions (test_sim.py:97-140)."""
+    args, meta = _mm_args(), dict(MM_META)
+    if mutate == "missing_meta":
+        del meta["BLOCK_SIZE_K"]
+    elif mutate == "zero_meta":
+        meta["BLOCK_SIZE_M"] = 0
+    elif mutate == "extra_meta":
+        meta["BLOCK"] = 3
+    elif mutate == "missing_arg":
+        del args["other"]
+    elif mutate == "extra_arg":
+        args["bias"] = _Fake((4,))
+    elif mutate == "wrong_rank":
+        args["other"] = _Fake((4,))
+    elif mutate == "bad_check":
+        args["output"] = _Fake((9, 4))
+    with pytest.raises(backend.LaunchError):
+        backend.launch(C.checked("mm"), args, meta)
+
+
+def test_rms_norm_padded_width_check():
+    args = {"input": _Fake((3, 20)), "weight": _Fake((20,)), "output": _Fake((3, 20))}
+    with pytest.raises(backend.LaunchError, match="launch-time check failed"):
+        backend.launch(C.checked("rms_norm"), args, {"COLS_PADDED": 16})
+
+
+def test_non_catalog_spec_is_rejected():
+    from paper_2507_11978_b200.spec import KernelSpec, ParamSpec, Store, Load, typecheck, ArrangeOp
+    spec = KernelSpec("add", (ParamSpec("input", 1, "f32", "in"), ParamSpec("output", 1, "f32", "out")),
+                      ("BLOCK_SIZE",),
+                      {"input": (ArrangeOp("tile", shape=(S.var("BLOCK_SIZE"),)),),
+                       "output": (ArrangeOp("tile", shape=(S.var("BLOCK_SIZE"),)),)},
+                      (Store("output", Load("input")),))
+    with pytest.raises(backend.UnsupportedSpecError):
+        backend.launch(typecheck(spec), {"input": _Fake((8,)), "output": _Fake((8,))},
+                       {"BLOCK_SIZE": 4})
