@@ -244,31 +244,43 @@ def build_works(dev, which):
     return {k: works[k] for k in which}
 
 
-def time_work(work, steps, warmup, n_gpus):
-    """Device time per call (ms) with CUDA events on the launch stream."""
+def _graph(fn, steps):
+    """Capture `steps` calls of fn(i) into one CUDA graph (device-side timing
+    without host launch overhead; the captured kernels are the native ones)."""
     import torch
 
     from paper_2507_11978_b200 import backend as B
 
+    g = torch.cuda.CUDAGraph()
+    n0 = B.launch_count()
+    with torch.cuda.graph(g):
+        for i in range(steps):
+            fn(i)
+    return g, B.launch_count() - n0
+
+
+def time_work(work, steps, warmup, n_gpus):
+    """Device time per call (ms): `steps` calls captured in a CUDA graph,
+    one replay timed with CUDA events on the launch stream."""
+    import torch
+
     sets = work.setup()
-    stream = torch.cuda.current_stream()
     for i in range(warmup):
         work.call(sets[i % len(sets)])
+    torch.cuda.synchronize()
+    g, launches = _graph(lambda i: work.call(sets[i % len(sets)]), steps)
+    g.replay()
     _barrier(n_gpus)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
-    n0 = B.launch_count()
-    for i in range(steps):
-        starts[i].record(stream)
-        work.call(sets[i % len(sets)])
-        ends[i].record(stream)
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    g.replay()
+    t1.record(stream)
     _barrier(n_gpus)
-    launches = B.launch_count() - n0
-    per = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total = starts[0].elapsed_time(ends[-1])
-    del sets
+    total = t0.elapsed_time(t1)
+    del g, sets
     torch.cuda.empty_cache()
-    return statistics.mean(per), total, launches, per
+    return total / steps, total, launches
 
 
 def _roofline(work, ms, pk, traffic):
@@ -302,35 +314,38 @@ def headline(args, n_gpus, rank, pk):
     sets = [dict(xa=U((R, C)), xb=U((R, C)), ya=torch.empty((R, C), device=dev, dtype=f16),
                  yb=torch.empty((R, C), device=dev, dtype=f16)) for _ in range(nsets)]
     stream = torch.cuda.current_stream()
-    ev = {k: [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-          for k in ("s0", "s1", "s2")}
 
-    def step(s, i=None):
-        if i is not None:
-            ev["s0"][i].record(stream)
-        B.softmax_launch(s["xa"], s["ya"], C)
-        if i is not None:
-            ev["s1"][i].record(stream)
-        B.rms_norm_launch(s["xb"], w, s["yb"], C)
-        if i is not None:
-            ev["s2"][i].record(stream)
+    def step(i):
+        s_ = sets[i % nsets]
+        B.softmax_launch(s_["xa"], s_["ya"], C)
+        B.rms_norm_launch(s_["xb"], w, s_["yb"], C)
 
     for i in range(args.warmup):
-        step(sets[i % nsets])
+        step(i)
+    torch.cuda.synchronize()
+    g_step, launches = _graph(step, args.steps)
+    g_sm, _ = _graph(lambda i: B.softmax_launch(sets[i % nsets]["xa"], sets[i % nsets]["ya"], C),
+                     args.steps)
+    g_rms, _ = _graph(lambda i: B.rms_norm_launch(sets[i % nsets]["xb"], w, sets[i % nsets]["yb"], C),
+                      args.steps)
+    for gr in (g_step, g_sm, g_rms):
+        gr.replay()
     _barrier(n_gpus)
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n0 = B.launch_count()
-    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
-        t0.record(stream)
-        for i in range(args.steps):
-            step(sets[i % nsets], i)
-        t1.record(stream)
+
+    def timed(gr):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         _barrier(n_gpus)
-    launches = B.launch_count() - n0
-    ms_total = _max_over_ranks(t0.elapsed_time(t1), n_gpus)
+        a.record(stream)
+        gr.replay()
+        b.record(stream)
+        _barrier(n_gpus)
+        return a.elapsed_time(b)
+
+    ms_total = _max_over_ranks(timed(g_step), n_gpus)
+    sm_ms = timed(g_sm) / args.steps
+    rms_ms = timed(g_rms) / args.steps
+    del g_step, g_sm, g_rms
     ms_step = ms_total / args.steps
-    sm_ms = statistics.mean(ev["s0"][i].elapsed_time(ev["s1"][i]) for i in range(args.steps))
-    rms_ms = statistics.mean(ev["s1"][i].elapsed_time(ev["s2"][i]) for i in range(args.steps))
     value = n_gpus * step_bytes / (ms_step * 1e-3) / 1e9
 
     # verification (after timing): per-rank error on sampled rows, one gather
@@ -396,7 +411,7 @@ def headline(args, n_gpus, rank, pk):
             "frac": round(dom_units / (dom_ms * 1e-3) / 1e9 / pk["hbm"], 4),
             "traffic": traffic, "peak_source": pk["src"],
             "per_kernel_ms": {"softmax": round(sm_ms, 5), "rms_norm": round(rms_ms, 5)}}
-    return dict(value=value, ms_step=ms_step, launches=launches, clocks=clk.summary(),
+    return dict(value=value, ms_step=ms_step, launches=launches,
                 e2e=e2e, roofline=roof, errs=errs, nsets=nsets)
 
 
@@ -460,6 +475,12 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def B_paths():
+    from paper_2507_11978_b200 import backend
+
+    return {k: v for k, v in backend.path_counts().items() if v}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -479,6 +500,7 @@ def main():
     n_gpus, rank, local = _dist()
     torch.cuda.set_device(local)
     pk = peaks()
+    clk = Clocks(local).__enter__()
     h = headline(args, n_gpus, rank, pk)
     kernels = {}
     names = ["add_2^20", "add_2^24", "silu_2^24", "softmax", "rms_norm", "mm", "addmm", "bmm",
@@ -491,7 +513,7 @@ def main():
         for key, wk in works.items():
             try:
                 steps = args.kernel_steps if wk.bound == "hbm" or key not in ("sdpa",) else 3
-                ms, total, launches, per = time_work(wk, steps, 2, n_gpus)
+                ms, total, launches = time_work(wk, steps, 2, n_gpus)
                 ms = _max_over_ranks(ms, n_gpus)
                 kernels[key] = {"workload": wk.name, "ms": round(ms, 5),
                                 "launches": launches,
@@ -499,6 +521,8 @@ def main():
                                 "note": wk.note}
             except Exception as e:  # report, never hide
                 kernels[key] = {"workload": wk.name, "error": f"{type(e).__name__}: {e}"}
+    clk.__exit__(None, None, None)
+    h["clocks"] = clk.summary()
     if rank != 0:
         return
     line = {
@@ -513,6 +537,7 @@ def main():
         "roofline": h["roofline"], "cpu_baseline": cpu_baseline(),
         "verify": {"max_err_per_rank": h["errs"], "gather": "one all_gather after timing" if n_gpus > 1 else "local"},
         "kernels": kernels,
+        "native_paths": B_paths(),
     }
     print(json.dumps(line), flush=True)
     if n_gpus > 1:

@@ -70,6 +70,20 @@ const char* ntb_last_error(void);
 /* Number of kernels launched by this library since load (all threads). */
 int64_t ntb_launch_count(void);
 
+/* Launches per execution path since load (evidence of which kernel ran). */
+enum {
+  NTB_PATH_PROBE = 0,
+  NTB_PATH_EW_VEC = 1, NTB_PATH_EW_GENERIC = 2,
+  NTB_PATH_ROW_VEC = 3, NTB_PATH_ROW_GENERIC = 4,
+  NTB_PATH_ROPE_VEC = 5, NTB_PATH_ROPE_GENERIC = 6,
+  NTB_PATH_GEMM_TC = 7, NTB_PATH_GEMM_GENERIC = 8,
+  NTB_PATH_CONV_TC = 9, NTB_PATH_CONV_GENERIC = 10,
+  NTB_PATH_ATTN_TC = 11, NTB_PATH_ATTN_GENERIC = 12,
+  NTB_PATH_REPACK = 13,
+  NTB_NUM_PATHS = 14
+};
+int64_t ntb_path_count(int path);
+
 /* ---- map VM: expressions ------------------------------------------------
  * An expression is postfix int64 code:
  *   0 k : push constant k      1 i : push slots[i]

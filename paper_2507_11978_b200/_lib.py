@@ -19,7 +19,8 @@ KERNEL_IDS = {"add": 1, "silu": 2, "softmax": 3, "rms_norm": 4, "mm": 5, "bmm": 
               "addmm": 7, "conv2d": 8, "sdpa": 9, "rope": 10}
 
 # every symbol include/ntb200.h declares (checked by tests/test_abi.py)
-EXPORTS = ("ntb_abi_version", "ntb_last_error", "ntb_launch_count", "ntb_expr_eval",
+EXPORTS = ("ntb_abi_version", "ntb_last_error", "ntb_launch_count", "ntb_path_count",
+           "ntb_expr_eval",
            "ntb_grid_eval", "ntb_map_enumerate", "ntb_map_probe", "ntb_launch",
            "ntb_release_workspace")
 
@@ -45,6 +46,8 @@ def lib():
     L.ntb_abi_version.restype = ctypes.c_int
     L.ntb_last_error.restype = ctypes.c_char_p
     L.ntb_launch_count.restype = ctypes.c_int64
+    L.ntb_path_count.restype = ctypes.c_int64
+    L.ntb_path_count.argtypes = [ctypes.c_int]
     L.ntb_expr_eval.argtypes = [_i64p, ctypes.c_int64, _i64p, ctypes.c_int64, _i64p]
     L.ntb_grid_eval.argtypes = [_i64p, ctypes.c_int64, _i64p, ctypes.c_int64, _i64p,
                                 ctypes.c_int64, _i64p]
@@ -106,6 +109,15 @@ def map_enumerate(blob: np.ndarray, param: int, slots: np.ndarray):
     rc = L.ntb_map_enumerate(i64(blob), len(blob), param, i64(slots), len(slots), i64(offs),
                              u8(mask), cnt, i64(n))
     return rc, offs, mask
+
+
+PATHS = ("probe", "ew_vec", "ew_generic", "row_vec", "row_generic", "rope_vec", "rope_generic",
+         "gemm_tc", "gemm_generic", "conv_tc", "conv_generic", "attn_tc", "attn_generic", "repack")
+
+
+def path_counts() -> dict:
+    L = lib()
+    return {name: int(L.ntb_path_count(i)) for i, name in enumerate(PATHS)}
 
 
 def loaded_path() -> str:

@@ -177,8 +177,63 @@ def evaluate_grid(checked, binding: dict) -> tuple:
     return grid
 
 
+_plans: dict = {}
+_PLAN_CAP = 4096
+
+
+def _plan_key(checked, args: Mapping, meta: Mapping):
+    parts = [id(checked)]
+    for k in sorted(meta):
+        parts.append((k, meta[k]))
+    for k in sorted(args):
+        v = args[k]
+        if hasattr(v, "shape") and hasattr(v, "stride") and len(v.shape) == 0:
+            parts.append((k, float(v.item())))
+        elif hasattr(v, "shape") and hasattr(v, "stride"):
+            parts.append((k, tuple(v.shape), tuple(v.stride()), getattr(v, "dtype", None),
+                          getattr(v, "device", None), type(v)))
+        else:
+            try:
+                parts.append((k, float(v)))
+            except (TypeError, ValueError):
+                parts.append((k, id(v)))
+    return tuple(parts)
+
+
 def launch(checked, args: Mapping, meta: Mapping, *, stream=None) -> LaunchResult:
-    """Execute a CheckedSpec on the current CUDA device (sim.launch twin)."""
+    """Execute a CheckedSpec on the current CUDA device (sim.launch twin).
+
+    The first call for a given (spec, shapes, strides, dtype, meta, scalars)
+    validates, evaluates checks and grid through the native map VM and
+    prebuilds the C-ABI argument block; later calls with the same signature
+    only swap the data pointers (host overhead of a few microseconds).
+    """
+    import torch
+
+    key = _plan_key(checked, args, meta)
+    plan = _plans.get(key)
+    if plan is None or plan[0] is not checked:
+        plan = (checked,) + _make_plan(checked, args, meta)
+        if len(_plans) > _PLAN_CAP:
+            _plans.clear()
+        _plans[key] = plan
+    _, names, kid, dt, n, sizes, strides, ranks, metas, sc, n_sc, result, dev = plan
+    ptrs = (ctypes.c_void_p * n)(*[args[nm].data_ptr() for nm in names])
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        rc = _lib.lib().ntb_launch(kid, dt, ptrs, n, sc, n_sc, _lib.i64(sizes), _lib.i64(strides),
+                                   ranks, _lib.i64(metas), len(metas), ctypes.c_void_p(stream))
+    if rc == _lib.NTB_ERR_UNSUPPORTED:
+        raise UnsupportedSpecError(_lib.last_error())
+    if rc == _lib.NTB_ERR_ARG or rc == _lib.NTB_ERR_CHECK:
+        raise LaunchError(_lib.last_error())
+    if rc:
+        raise BackendError(_lib.last_error())
+    return result
+
+
+def _make_plan(checked, args: Mapping, meta: Mapping):
     import torch
 
     spec = checked.spec
@@ -203,36 +258,31 @@ def launch(checked, args: Mapping, meta: Mapping, *, stream=None) -> LaunchResul
     for p, t in zip(tensors, ts):
         if _dtype_code(t) != dt:
             raise LaunchError(f"argument {p.name!r} has dtype {t.dtype}, expected {ts[0].dtype}")
+        if t.device != ts[0].device:
+            raise LaunchError(f"argument {p.name!r} is on {t.device}, expected {ts[0].device}")
     scalars = []
     for p in spec.params:
         if p.rank == 0:
             v = args[p.name]
             scalars.append(float(v.item() if hasattr(v, "item") else v))
     n = len(ts)
-    ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for t in ts])
     sizes = np.array([s for t in ts for s in t.shape], dtype=np.int64)
     strides = np.array([s for t in ts for s in t.stride()], dtype=np.int64)
     ranks = (ctypes.c_int * n)(*[t.dim() for t in ts])
     metas = np.array([binding[m] for m in spec.meta], dtype=np.int64)
     sc = (ctypes.c_double * max(1, len(scalars)))(*scalars)
-    if stream is None:
-        stream = torch.cuda.current_stream(ts[0].device).cuda_stream
-    with torch.cuda.device(ts[0].device):
-        rc = _lib.lib().ntb_launch(
-            _lib.KERNEL_IDS[family], dt, ptrs, n, sc, len(scalars), _lib.i64(sizes),
-            _lib.i64(strides), ranks, _lib.i64(metas), len(metas), ctypes.c_void_p(stream))
-    if rc == _lib.NTB_ERR_UNSUPPORTED:
-        raise UnsupportedSpecError(_lib.last_error())
-    if rc == _lib.NTB_ERR_ARG or rc == _lib.NTB_ERR_CHECK:
-        raise LaunchError(_lib.last_error())
-    if rc:
-        raise BackendError(_lib.last_error())
-    return LaunchResult(grid=tuple(grid), total=total)
+    return ([p.name for p in tensors], _lib.KERNEL_IDS[family], dt, n, sizes, strides, ranks,
+            metas, sc, len(scalars), LaunchResult(grid=tuple(grid), total=total), ts[0].device)
 
 
 def launch_count() -> int:
     """Kernels launched by libntb200 in this process."""
     return int(_lib.lib().ntb_launch_count())
+
+
+def path_counts() -> dict:
+    """Launches per native execution path (tcgen05 vs generic, ...)."""
+    return _lib.path_counts()
 
 
 # ---- emitted-launcher twins (emit.py:267-293) ------------------------------

@@ -104,13 +104,14 @@ static int run_ew(const LaunchArgs& A) {
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     ew_vec_kernel<T, Op, U><<<(unsigned)blocks, 256, 0, A.stream>>>(a, b, out, n_vec);
+    return check_launch("elementwise", NTB_PATH_EW_VEC);
   } else {
     int64_t blocks = cdiv64(no, 256);
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
     ew_generic_kernel<T, Op><<<(unsigned)blocks, 256, 0, A.stream>>>(a, na, sa, b, nb, sb, out,
                                                                       no, so);
   }
-  return check_launch("elementwise");
+  return check_launch("elementwise", NTB_PATH_EW_GENERIC);
 }
 
 int launch_elementwise(const LaunchArgs& A) {

@@ -75,7 +75,7 @@ template <typename T>
 static int gemm_generic_t(const GemmDesc& g, cudaStream_t s) {
   dim3 grid((unsigned)cdiv64(g.c_n, GT), (unsigned)cdiv64(g.c_m, GT), (unsigned)g.batch);
   gemm_generic_kernel<T><<<grid, 256, 0, s>>>(g);
-  return check_launch("gemm generic");
+  return check_launch("gemm generic", NTB_PATH_GEMM_GENERIC);
 }
 
 int gemm_generic(const GemmDesc& g, int dtype, cudaStream_t s) {
@@ -159,7 +159,7 @@ int conv_generic(const ConvDesc& c, int dtype, cudaStream_t s) {
     case NTB_BF16: conv_generic_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(c); break;
     default: return fail(NTB_ERR_UNSUPPORTED, "conv2d: unsupported dtype");
   }
-  return check_launch("conv2d generic");
+  return check_launch("conv2d generic", NTB_PATH_CONV_GENERIC);
 }
 
 // ---- attention: one warp per query row, online softmax in fp32 ----------
@@ -217,7 +217,7 @@ static int attn_generic_t(const AttnDesc& a, cudaStream_t s) {
   else if (a.D <= 128) attn_generic_kernel<T, 4><<<blocks, 128, 0, s>>>(a);
   else if (a.D <= 256) attn_generic_kernel<T, 8><<<blocks, 128, 0, s>>>(a);
   else return fail(NTB_ERR_UNSUPPORTED, "sdpa: head dim > 256");
-  return check_launch("sdpa generic");
+  return check_launch("sdpa generic", NTB_PATH_ATTN_GENERIC);
 }
 
 int attn_generic(const AttnDesc& a, int dtype, cudaStream_t s) {

@@ -120,6 +120,7 @@ static int run_rope(const LaunchArgs& A) {
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
     rope_vec_kernel<T><<<(unsigned)blocks, 256, 0, A.stream>>>(x, sn, cs, out, rows, xs.n[1],
                                                                xs.n[2], (int)half);
+    return check_launch("rope", NTB_PATH_ROPE_VEC);
   } else {
     int64_t items = xs.n[1] * xs.n[0] * xs.n[2] * half;
     int64_t blocks = cdiv64(items, 256);
@@ -128,7 +129,7 @@ static int run_rope(const LaunchArgs& A) {
         x, xs, sn, st[sb], st[sb + 1], sz[sb + 1], cs, st[cb], st[cb + 1], sz[cb + 1], out, os,
         half);
   }
-  return check_launch("rope");
+  return check_launch("rope", NTB_PATH_ROPE_GENERIC);
 }
 
 int launch_rope(const LaunchArgs& A) {

@@ -221,7 +221,7 @@ static int run_rows(const LaunchArgs& A) {
   if (fast) {
     bool ok = softmax ? try_vec<T, true>(in, irs, nullptr, out, ors, R, C, A.stream)
                       : try_vec<T, false>(in, irs, w, out, ors, R, C, A.stream);
-    if (ok) return check_launch("rowwise vec");
+    if (ok) return check_launch("rowwise vec", NTB_PATH_ROW_VEC);
   }
   int threads = 256;
   if (softmax) {
@@ -233,7 +233,7 @@ static int run_rows(const LaunchArgs& A) {
     rms_generic_kernel<T><<<(unsigned)R, threads, 0, A.stream>>>(in, C, irs, ics, w, wn, ws, out,
                                                                  OC, ors, ocs, cp);
   }
-  return check_launch("rowwise generic");
+  return check_launch("rowwise generic", NTB_PATH_ROW_GENERIC);
 }
 
 int launch_rowwise(const LaunchArgs& A) {

@@ -14,6 +14,7 @@ namespace ntb {
 
 static thread_local std::string g_err;
 static std::atomic<int64_t> g_launches{0};
+static std::atomic<int64_t> g_paths[NTB_NUM_PATHS];
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -27,10 +28,11 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 void note_launch(int n) { g_launches += n; }
 
-int check_launch(const char* what) {
+int check_launch(const char* what, int path) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, what);
   note_launch();
+  if (path >= 0 && path < NTB_NUM_PATHS) g_paths[path]++;
   return NTB_OK;
 }
 
@@ -104,6 +106,11 @@ int ntb_abi_version(void) { return NTB_ABI_VERSION; }
 const char* ntb_last_error(void) { return g_err.c_str(); }
 
 int64_t ntb_launch_count(void) { return g_launches.load(); }
+
+int64_t ntb_path_count(int path) {
+  if (path < 0 || path >= NTB_NUM_PATHS) return -1;
+  return g_paths[path].load();
+}
 
 int ntb_expr_eval(const int64_t* code, int64_t code_len, const int64_t* slots,
                   int64_t n_slots, int64_t* out) {
@@ -242,7 +249,7 @@ int ntb_map_probe(const int64_t* blob, int64_t blob_len, int param, const int64_
   map_probe_kernel<<<(unsigned)blocks, threads, 0, s>>>(
       dbuf, blob_len, param, dbuf + blob_len, n_slots, dbuf + blob_len + n_slots,
       dbuf + blob_len + n_slots + 8, n, d_offs, d_mask, (int*)(dbuf + words - 1));
-  if ((rc = check_launch("map probe"))) return rc;
+  if ((rc = check_launch("map probe", NTB_PATH_PROBE))) return rc;
   int64_t status = 0;
   e = cudaMemcpyAsync(&status, dbuf + words - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);

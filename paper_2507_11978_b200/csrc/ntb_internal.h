@@ -18,7 +18,7 @@ void note_launch(int n = 1);
 int sm_count();
 
 // Check the last launch and return NTB_OK / NTB_ERR_CUDA.
-int check_launch(const char* what);
+int check_launch(const char* what, int path = -1);
 
 // Per-family unpacked arguments (element strides).
 struct Tensor1 { void* p; int64_t n, s; };

@@ -95,6 +95,18 @@ def test_fp32_matches_reference_simulator(kernel):
     assert n >= 20
 
 
+class _Paths:
+    """Delta of native path launch counters across a block."""
+
+    def __enter__(self):
+        self.before = backend.path_counts()
+        return self
+
+    def __exit__(self, *exc):
+        after = backend.path_counts()
+        self.delta = {k: after[k] - self.before[k] for k in after}
+
+
 def _close(got, ref, rtol=1e-2, atol=1e-2):
     got = got.float().cpu().numpy().astype(np.float64)
     bad = np.abs(got - ref) > atol + rtol * np.abs(ref)
@@ -160,7 +172,9 @@ def test_mm_half(dtype, mnk):
     a = _r16(rng.uniform(-1, 1, (m, k)).astype(np.float32), dtype)
     b = _r16(rng.uniform(-1, 1, (k, n)).astype(np.float32), dtype)
     meta = {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128, "BLOCK_SIZE_K": 64}
-    got = _run("mm", {"input": a, "other": b}, meta, dtype)
+    with _Paths() as pc:
+        got = _run("mm", {"input": a, "other": b}, meta, dtype)
+    assert pc.delta["gemm_tc"] == 1 and pc.delta["gemm_generic"] == 0
     rows = np.arange(m) if m <= 1024 else rng.choice(m, 256, replace=False)
     ref = oracle.mm(a[rows], b)
     _close(got[torch.as_tensor(rows, device=DEV)], ref, rtol=1e-2, atol=2e-2)
@@ -174,7 +188,9 @@ def test_mm_transposed_operands(dtype):
     b = _r16(rng.uniform(-1, 1, (n, k)).astype(np.float32), dtype)
     ta, tb = _t(a, dtype).t(), _t(b, dtype).t()     # M-major A, N-major... views
     meta = {"BLOCK_SIZE_M": 64, "BLOCK_SIZE_N": 64, "BLOCK_SIZE_K": 32}
-    got = _run("mm", {"input": ta, "other": tb}, meta, dtype)
+    with _Paths() as pc:
+        got = _run("mm", {"input": ta, "other": tb}, meta, dtype)
+    assert pc.delta["gemm_tc"] == 1
     _close(got, oracle.mm(a.T, b.T), rtol=1e-2, atol=2e-2)
 
 
@@ -199,7 +215,9 @@ def test_bmm_half(dtype, bmnk):
     a = _r16(rng.uniform(-1, 1, (bt, m, k)).astype(np.float32), dtype)
     b = _r16(rng.uniform(-1, 1, (bt, k, n)).astype(np.float32), dtype)
     meta = {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128, "BLOCK_SIZE_K": 64}
-    got = _run("bmm", {"input": a, "other": b}, meta, dtype)
+    with _Paths() as pc:
+        got = _run("bmm", {"input": a, "other": b}, meta, dtype)
+    assert pc.delta["gemm_tc"] == 1
     sel = [0, bt - 1]
     _close(got[sel], oracle.bmm(a[sel], b[sel]), rtol=1e-2, atol=2e-2)
 
@@ -257,6 +275,34 @@ def test_rope(dtype, shape):
     got = _run("rope", {"input": x, "sin": sn, "cos": cs}, {"HALF_D": d // 2}, dtype, out=out)
     tol = 1e-5 if dtype == torch.float32 else 1e-2
     _close(got, oracle.rope(x, sn, cs), rtol=tol, atol=tol)
+
+
+@pytest.mark.parametrize("dtype", DTS)
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+def test_mm_all_operand_majors(dtype, a_mn, b_mn):
+    """K-major / MN-major A and B (every UMMA descriptor combination)."""
+    rng = np.random.default_rng(17)
+    m, n, k = 320, 288, 192
+    a = _r16(rng.uniform(-1, 1, (m, k)).astype(np.float32), dtype)
+    b = _r16(rng.uniform(-1, 1, (k, n)).astype(np.float32), dtype)
+    ta = _t(a.T.copy(), dtype).t() if a_mn else _t(a, dtype)
+    tb = _t(b, dtype) if b_mn else _t(b.T.copy(), dtype).t()
+    with _Paths() as pc:
+        got = _run("mm", {"input": ta, "other": tb}, {"BLOCK_SIZE_M": 16, "BLOCK_SIZE_N": 16,
+                                                      "BLOCK_SIZE_K": 16}, dtype)
+    assert pc.delta["gemm_tc"] == 1
+    _close(got, oracle.mm(a, b), rtol=1e-2, atol=2e-2)
+
+
+def test_mm_unaligned_takes_generic_gpu_path():
+    rng = np.random.default_rng(2)
+    a = rng.uniform(-1, 1, (33, 13)).astype(np.float16).astype(np.float32)
+    b = rng.uniform(-1, 1, (13, 7)).astype(np.float16).astype(np.float32)
+    with _Paths() as pc:
+        got = _run("mm", {"input": a, "other": b}, {"BLOCK_SIZE_M": 16, "BLOCK_SIZE_N": 16,
+                                                    "BLOCK_SIZE_K": 16}, torch.float16)
+    assert pc.delta["gemm_generic"] == 1
+    _close(got, oracle.mm(a, b), rtol=1e-2, atol=1e-2)
 
 
 def test_launch_counter_proves_native_path():
