@@ -80,7 +80,8 @@ enum {
   NTB_PATH_CONV_TC = 9, NTB_PATH_CONV_GENERIC = 10,
   NTB_PATH_ATTN_TC = 11, NTB_PATH_ATTN_GENERIC = 12,
   NTB_PATH_REPACK = 13,
-  NTB_NUM_PATHS = 14
+  NTB_PATH_ROW_STREAM = 14,
+  NTB_NUM_PATHS = 15
 };
 int64_t ntb_path_count(int path);
 

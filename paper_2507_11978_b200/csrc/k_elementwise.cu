@@ -21,7 +21,7 @@ struct AddOp {
 struct SiluOp {
   static constexpr int kIn = 1;
   __device__ __forceinline__ float operator()(float x, float) const {
-    return x / (1.0f + expf(-x));
+    return __fdividef(x, 1.0f + exp2f(-x * 1.4426950408889634f));
   }
 };
 

@@ -24,6 +24,7 @@
 // Tensor roofline: 2*M*N*K flop per launch (x batch).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "k_sm100.cuh"
@@ -89,6 +90,87 @@ template <bool BF16>
 __device__ __forceinline__ void store_el(void* p, int64_t i, float v) {
   if constexpr (BF16) reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v);
   else reinterpret_cast<__half*>(p)[i] = __float2half_rn(v);
+}
+
+
+// One accumulator row (this thread's TMEM lane) of a 256-column tile:
+// tcgen05.ld 32 columns at a time, fp32 epilogue (alpha*acc + beta*addend),
+// convert, 128-bit stores when the row segment is aligned.
+template <bool BF16>
+__device__ __forceinline__ void epilogue_row(const GemmParams& p, uint32_t taddr, int b, int row,
+                                             int col_base) {
+  using namespace sm100;
+  char* cbase = reinterpret_cast<char*>(p.c) + (int64_t)b * p.c_sb * 2;
+#pragma unroll 1
+  for (int cc = 0; cc < 256 / 32; ++cc) {
+    uint32_t v[32];
+    __syncwarp();
+    tmem_ld_32x32b_x32(taddr + cc * 32, v);
+    tmem_ld_wait();
+    const int col0 = col_base + cc * 32;
+    if (row < p.M && col0 < p.N) {
+      float f[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
+      if (p.has_d) {
+        const bool dvec = p.d_sn == 1 && row < p.d_m && col0 + 32 <= p.d_n && (p.d_sm % 8) == 0 &&
+                          ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0);
+        if (dvec) {
+          const uint4* dp = reinterpret_cast<const uint4*>(
+              reinterpret_cast<const char*>(p.d) + ((int64_t)row * p.d_sm + col0) * 2);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u = dp[q];
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float lo, hi;
+              if constexpr (BF16) {
+                __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[e]);
+                lo = __low2float(h);
+                hi = __high2float(h);
+              } else {
+                __half2 h = *reinterpret_cast<const __half2*>(&w[e]);
+                lo = __low2float(h);
+                hi = __high2float(h);
+              }
+              f[q * 8 + e * 2] += p.beta * lo;
+              f[q * 8 + e * 2 + 1] += p.beta * hi;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int col = col0 + i;
+            const float dv = (row < p.d_m && col < p.d_n)
+                                 ? load_el<BF16>(p.d, (int64_t)row * p.d_sm + (int64_t)col * p.d_sn)
+                                 : 0.f;
+            f[i] += p.beta * dv;
+          }
+        }
+      }
+      const bool cvec = p.c_sn == 1 && col0 + 32 <= p.N && (p.c_sm % 8) == 0 &&
+                        ((reinterpret_cast<uintptr_t>(cbase) & 15) == 0);
+      if (cvec) {
+        uint4* cp = reinterpret_cast<uint4*>(cbase + ((int64_t)row * p.c_sm + col0) * 2);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            w[e] = BF16 ? pack_bf16(f[q * 8 + e * 2], f[q * 8 + e * 2 + 1])
+                        : pack_f16(f[q * 8 + e * 2], f[q * 8 + e * 2 + 1]);
+          cp[q] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < p.N)
+            store_el<BF16>(cbase, (int64_t)row * p.c_sm + (int64_t)(col0 + i) * p.c_sn, f[i]);
+      }
+    }
+  }
+  __syncwarp();
 }
 
 template <bool A_MN, bool B_MN, bool BF16>
@@ -209,74 +291,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const int row = mt * BM + ew * 32 + lane;
-      char* cbase = reinterpret_cast<char*>(p.c) + (int64_t)b * p.c_sb * 2;
-#pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        uint32_t v[32];
-        __syncwarp();
-        tmem_ld_32x32b_x32(tmem_base + acc * BN + cc * 32 + ((uint32_t)(ew * 32) << 16), v);
-        tmem_ld_wait();
-        const int col0 = nt * BN + cc * 32;
-        if (row < p.M && col0 < p.N) {
-        float f[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
-        if (p.has_d) {
-          const bool dvec = p.d_sn == 1 && row < p.d_m && col0 + 32 <= p.d_n && (p.d_sm % 8) == 0 &&
-                            ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0);
-          if (dvec) {
-            const uint4* dp = reinterpret_cast<const uint4*>(
-                reinterpret_cast<const char*>(p.d) + ((int64_t)row * p.d_sm + col0) * 2);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 u = dp[q];
-              const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float lo, hi;
-                if constexpr (BF16) {
-                  __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[e]);
-                  lo = __low2float(h);
-                  hi = __high2float(h);
-                } else {
-                  __half2 h = *reinterpret_cast<const __half2*>(&w[e]);
-                  lo = __low2float(h);
-                  hi = __high2float(h);
-                }
-                f[q * 8 + e * 2] += p.beta * lo;
-                f[q * 8 + e * 2 + 1] += p.beta * hi;
-              }
-            }
-          } else {
-            for (int i = 0; i < 32; ++i) {
-              const int col = col0 + i;
-              const float dv = (row < p.d_m && col < p.d_n)
-                                   ? load_el<BF16>(p.d, (int64_t)row * p.d_sm + (int64_t)col * p.d_sn)
-                                   : 0.f;
-              f[i] += p.beta * dv;
-            }
-          }
-        }
-        const bool cvec = p.c_sn == 1 && col0 + 32 <= p.N && (p.c_sm % 8) == 0 &&
-                          ((reinterpret_cast<uintptr_t>(cbase) & 15) == 0);
-        if (cvec) {
-          uint4* cp = reinterpret_cast<uint4*>(cbase + ((int64_t)row * p.c_sm + col0) * 2);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              w[e] = BF16 ? pack_bf16(f[q * 8 + e * 2], f[q * 8 + e * 2 + 1])
-                          : pack_f16(f[q * 8 + e * 2], f[q * 8 + e * 2 + 1]);
-            cp[q] = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        } else {
-          for (int i = 0; i < 32 && col0 + i < p.N; ++i)
-            store_el<BF16>(cbase, (int64_t)row * p.c_sm + (int64_t)(col0 + i) * p.c_sn, f[i]);
-        }
-        }
-      }
-      __syncwarp();
+      epilogue_row<BF16>(p, tmem_base + acc * BN + ((uint32_t)(ew * 32) << 16), b, row, nt * BN);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -304,6 +319,172 @@ int launch_tc(const GemmMaps& maps, const GemmParams& p, cudaStream_t s) {
   return check_launch("gemm tcgen05", NTB_PATH_GEMM_TC);
 }
 
+
+// ---- CTA-pair variant (cta_group::2): 256 x 256 tiles per 2-SM cluster ----
+// Each CTA of the pair TMA-loads half of A (128 rows) and half of B (128
+// rows of N) per 64-wide K step; CTA 0 issues tcgen05.mma.cta_group::2
+// (M = 256, N = 256) reading both CTAs' shared memory, so each SM streams
+// 32 KB per K step instead of 48 KB (the 1-CTA kernel sits at the L2->SM
+// bandwidth ceiling); both CTAs' TMA bytes complete on CTA 0's barrier, the
+// MMA commit multicasts stage-free / accumulator-ready to both CTAs, and the
+// epilogue warps of both CTAs release the accumulator on CTA 0's barrier.
+constexpr int PSTAGES = 6;
+constexpr int PA_BYTES = 128 * BK * 2;
+constexpr int PB_BYTES = 128 * BK * 2;
+constexpr int PSTAGE_BYTES = PA_BYTES + PB_BYTES;
+constexpr int PSMEM_BYTES = PSTAGES * PSTAGE_BYTES + 1024;
+
+template <bool A_MN, bool B_MN, bool BF16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_pair_kernel(const __grid_constant__ GemmMaps maps, const GemmParams p) {
+  using namespace sm100;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + PSTAGES * PA_BYTES;
+  __shared__ __align__(8) uint64_t full[PSTAGES], empty[PSTAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int tiles_per_batch = p.num_m * p.num_n;
+  const int total = tiles_per_batch * p.batch;
+  const int nk = (p.K + BK - 1) / BK;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PSTAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&maps.a);
+    tma_prefetch(&maps.b);
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(&tmem_slot, TMEM_COLS);
+    tc_fence_before();
+  }
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int t = cid; t < total; t += ncl) {
+        const int b = t / tiles_per_batch, r = t % tiles_per_batch;
+        const int nt = r / p.num_m, mt = r % p.num_m;
+        const int row = mt * 256 + (int)rank * 128, col = nt * 256 + (int)rank * 128;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[st], ph ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[st], 2 * PSTAGE_BYTES);
+          const uint32_t bar = leader_addr(&full[st]);
+          uint8_t* a_dst = sA + st * PA_BYTES;
+          uint8_t* b_dst = sB + st * PB_BYTES;
+          if (!A_MN) {
+            tma_load_3d_pair(a_dst, &maps.a, bar, kb * BK, row, b);
+          } else {
+            tma_load_3d_pair(a_dst, &maps.a, bar, row, kb * BK, b);
+            tma_load_3d_pair(a_dst + BK * 128, &maps.a, bar, row + 64, kb * BK, b);
+          }
+          if (!B_MN) {
+            tma_load_3d_pair(b_dst, &maps.b, bar, kb * BK, col, b);
+          } else {
+            tma_load_3d_pair(b_dst, &maps.b, bar, col, kb * BK, b);
+            tma_load_3d_pair(b_dst + BK * 128, &maps.b, bar, col + 64, kb * BK, b);
+          }
+          if (++st == PSTAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && elect_one()) {
+      constexpr uint32_t idesc = idesc_f16(BF16, A_MN, B_MN, 256, 256);
+      int st = 0;
+      uint32_t ph = 0;
+      int tl = 0;
+      for (int t = cid; t < total; t += ncl, ++tl) {
+        const int acc = tl & 1;
+        const uint32_t aph = (tl >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + st * PA_BYTES);
+          const uint32_t b_addr = smem_u32(sB + st * PB_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? umma_desc_sw128(a_addr + k * 2048, BK * 128, 1024)
+                                     : umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024)
+                                     : umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            mma_f16_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit_pair(&empty[st]);
+          if (++st == PSTAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int tl = 0;
+    for (int t = cid; t < total; t += ncl, ++tl) {
+      const int b = t / tiles_per_batch, r = t % tiles_per_batch;
+      const int nt = r / p.num_m, mt = r % p.num_m;
+      const int acc = tl & 1;
+      const uint32_t aph = (tl >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int row = mt * 256 + (int)rank * 128 + ew * 32 + lane;
+      epilogue_row<BF16>(p, tmem_base + acc * 256 + ((uint32_t)(ew * 32) << 16), b, row,
+                         nt * 256);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+    }
+  }
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, TMEM_COLS);
+  }
+}
+
+template <bool A_MN, bool B_MN, bool BF16>
+int launch_pair(const GemmMaps& maps, const GemmParams& p, cudaStream_t s) {
+  auto k = gemm_pair_kernel<A_MN, B_MN, BF16>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PSMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm pair smem attribute");
+    attr_set = true;
+  }
+  const int total = p.num_m * p.num_n * p.batch;
+  int clusters = sm_count() / 2;
+  if (total < clusters) clusters = total;
+  k<<<2 * clusters, 256, PSMEM_BYTES, s>>>(maps, p);
+  return check_launch("gemm tcgen05 pair", NTB_PATH_GEMM_TC);
+}
+
 bool ok_stride(int64_t elems) { return elems > 0 && (elems * 2) % 16 == 0; }
 
 }  // namespace
@@ -323,6 +504,11 @@ int gemm_sm100(const GemmDesc& g, int dtype, cudaStream_t s) {
   else if (g.b_sn == 1 && ok_stride(g.b_sk)) b_mn = true;
   else return NTB_ERR_UNSUPPORTED;
   if (g.batch > 1 && (!ok_stride(g.a_sb) || !ok_stride(g.b_sb))) return NTB_ERR_UNSUPPORTED;
+  static const bool pair_enabled = [] {
+    const char* e = getenv("NTB_GEMM_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  const bool pair = pair_enabled && g.c_m > 128;
 
   GemmMaps maps;
   {
@@ -346,7 +532,7 @@ int gemm_sm100(const GemmDesc& g, int dtype, cudaStream_t s) {
     uint32_t box[3];
     const int64_t b_rows_stride = b_mn ? g.b_sk : (g.b_n == 1 ? g.k : g.b_sn);
     if (!b_mn) {
-      dims[0] = g.k; dims[1] = g.b_n; box[0] = 64; box[1] = BN;
+      dims[0] = g.k; dims[1] = g.b_n; box[0] = 64; box[1] = pair ? 128 : BN;
     } else {
       dims[0] = g.b_n; dims[1] = g.k; box[0] = 64; box[1] = BK;
     }
@@ -376,6 +562,16 @@ int gemm_sm100(const GemmDesc& g, int dtype, cudaStream_t s) {
   p.alpha = g.alpha;
   p.beta = g.beta;
   p.has_d = g.d != nullptr;
+  if (pair) {
+    p.num_m = (int)cdiv64(g.c_m, 256);
+    p.num_n = (int)cdiv64(g.c_n, 256);
+    if (bf16) {
+      if (a_mn) return b_mn ? launch_pair<true, true, true>(maps, p, s) : launch_pair<true, false, true>(maps, p, s);
+      return b_mn ? launch_pair<false, true, true>(maps, p, s) : launch_pair<false, false, true>(maps, p, s);
+    }
+    if (a_mn) return b_mn ? launch_pair<true, true, false>(maps, p, s) : launch_pair<true, false, false>(maps, p, s);
+    return b_mn ? launch_pair<false, true, false>(maps, p, s) : launch_pair<false, false, false>(maps, p, s);
+  }
   if (bf16) {
     if (a_mn) return b_mn ? launch_tc<true, true, true>(maps, p, s) : launch_tc<true, false, true>(maps, p, s);
     return b_mn ? launch_tc<false, true, true>(maps, p, s) : launch_tc<false, false, true>(maps, p, s);

@@ -16,6 +16,8 @@
 // Generic path: one CTA per (row, chunk) over arbitrary element strides.
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace ntb {
@@ -103,6 +105,199 @@ __global__ void __launch_bounds__(256) row_vec_kernel(const T* __restrict__ in, 
       }
     }
   }
+}
+
+
+// ---- TMA-bulk row streaming (the B200 fast path) --------------------------
+// Persistent CTAs of 8 warps; every warp owns a private ring of S row
+// buffers in shared memory filled by cp.async.bulk (global -> shared, one
+// bulk copy per row, completion on a per-buffer mbarrier), so each SM keeps
+// 8 x (S-1) rows (>= 100 KB) in flight - enough to cover HBM latency at full
+// bandwidth.  The warp reduces its row out of shared memory (warp shuffles,
+// fp32) and writes the result with 128-bit streaming stores.
+constexpr int kStreamWarps = 8;
+constexpr int kStreamMaxStages = 8;
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src), "r"(bytes),
+      "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
+
+template <typename T, bool kSoftmax>
+__global__ void __launch_bounds__(kStreamWarps * 32, 1)
+    row_stream_kernel(const T* __restrict__ in, int64_t in_rs, const T* __restrict__ w,
+                      T* __restrict__ out, int64_t out_rs, int64_t rows, int cols, int stages) {
+  using P = Pack<T>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[kStreamWarps][kStreamMaxStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t row_bytes = (uint32_t)cols * sizeof(T);
+  const uint32_t row_pad = (row_bytes + 127u) & ~127u;
+  uint8_t* wbase = smem + (size_t)warp * stages * row_pad;
+  const T* wsh = nullptr;
+  if (!kSoftmax) {
+    // weight row once per CTA, after the per-warp rings
+    uint8_t* wdst = smem + (size_t)kStreamWarps * stages * row_pad;
+    for (int c = threadIdx.x; c < cols / P::N; c += blockDim.x)
+      reinterpret_cast<uint4*>(wdst)[c] = reinterpret_cast<const uint4*>(w)[c];
+    wsh = reinterpret_cast<const T*>(wdst);
+  }
+  if (lane == 0)
+    for (int s = 0; s < stages; ++s) bar_init(&bars[warp][s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  const int64_t step = (int64_t)gridDim.x * kStreamWarps;
+  const int64_t first = (int64_t)blockIdx.x * kStreamWarps + warp;
+  if (lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      const int64_t r = first + s * step;
+      if (r < rows) {
+        bar_expect(&bars[warp][s], row_bytes);
+        bulk_g2s(wbase + (size_t)s * row_pad, in + r * in_rs, row_bytes, &bars[warp][s]);
+      }
+    }
+  }
+  const int n_vec = cols / P::N;
+  int64_t k = 0;
+  for (int64_t r = first; r < rows; r += step, ++k) {
+    const int s = (int)(k % stages);
+    bar_wait(&bars[warp][s], (uint32_t)((k / stages) & 1));
+    const uint4* buf = reinterpret_cast<const uint4*>(wbase + (size_t)s * row_pad);
+    T* dst = out + r * out_rs;
+    if (kSoftmax) {
+      // pass 1: row max; pass 2: e = exp(x - m) written back in place (fp16
+      // for 16-bit rows, fp32 for fp32 rows) + row sum; pass 3: e / sum.
+      // One exponential per element (the SFU, not HBM, would otherwise bound).
+      using E = typename std::conditional<sizeof(T) == 4, float, __half>::type;
+      float m = -INFINITY;
+      for (int c = lane; c < n_vec; c += 32) {
+        P v;
+        v.raw = buf[c];
+        float f[P::N];
+        v.to_float(f);
+#pragma unroll
+        for (int e = 0; e < P::N; ++e) m = fmaxf(m, f[e]);
+      }
+      m = warp_max(m);
+      float sum = 0.f;
+      uint4* ebuf = const_cast<uint4*>(buf);
+      for (int c = lane; c < n_vec; c += 32) {
+        P v;
+        v.raw = buf[c];
+        float f[P::N];
+        v.to_float(f);
+#pragma unroll
+        for (int e = 0; e < P::N; ++e) {
+          f[e] = fast_exp(f[e] - m);
+          sum += f[e];
+        }
+        Pack<E> o;
+        o.from_float(f);
+        ebuf[c] = o.raw;
+      }
+      const float inv = 1.0f / warp_sum(sum);
+      for (int c = lane; c < n_vec; c += 32) {
+        Pack<E> v;
+        v.raw = buf[c];
+        float f[P::N];
+        v.to_float(f);
+#pragma unroll
+        for (int e = 0; e < P::N; ++e) f[e] *= inv;
+        P o;
+        o.from_float(f);
+        st_stream(dst + (int64_t)c * P::N, o.raw);
+      }
+    } else {
+      float ss = 0.f;
+      for (int c = lane; c < n_vec; c += 32) {
+        P v;
+        v.raw = buf[c];
+        float f[P::N];
+        v.to_float(f);
+#pragma unroll
+        for (int e = 0; e < P::N; ++e) ss = fmaf(f[e], f[e], ss);
+      }
+      const float rinv = 1.0f / sqrtf(warp_sum(ss) / (float)cols + kRmsEps);
+      const uint4* wv = reinterpret_cast<const uint4*>(wsh);
+      for (int c = lane; c < n_vec; c += 32) {
+        P v, g;
+        v.raw = buf[c];
+        g.raw = wv[c];
+        float f[P::N], gf[P::N];
+        v.to_float(f);
+        g.to_float(gf);
+#pragma unroll
+        for (int e = 0; e < P::N; ++e) f[e] = f[e] * rinv * gf[e];
+        P o;
+        o.from_float(f);
+        st_stream(dst + (int64_t)c * P::N, o.raw);
+      }
+    }
+    // release the buffer: all lanes done reading, then refill it
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t nr = r + (int64_t)stages * step;
+      if (nr < rows) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bar_expect(&bars[warp][s], row_bytes);
+        bulk_g2s(wbase + (size_t)s * row_pad, in + nr * in_rs, row_bytes, &bars[warp][s]);
+      }
+    }
+  }
+}
+
+template <typename T, bool kSoftmax>
+static bool try_stream(const T* in, int64_t in_rs, const T* w, T* out, int64_t out_rs,
+                       int64_t rows, int64_t cols, cudaStream_t s) {
+  constexpr int N = Pack<T>::N;
+  const int64_t row_bytes = cols * (int64_t)sizeof(T);
+  if (cols % N || (in_rs * (int64_t)sizeof(T)) % 16 || out_rs % N || !aligned16(in) ||
+      !aligned16(out) || (w && !aligned16(w)) || rows < 1)
+    return false;
+  const int64_t row_pad = (row_bytes + 127) & ~int64_t(127);
+  const int64_t budget = 200 * 1024 - (kSoftmax ? 0 : row_pad);
+  int64_t stages = budget / (kStreamWarps * row_pad);
+  if (stages > kStreamMaxStages) stages = kStreamMaxStages;
+  if (stages < 2) return false;
+  const size_t smem = (size_t)(kStreamWarps * stages * row_pad + (kSoftmax ? 0 : row_pad));
+  auto kern = row_stream_kernel<T, kSoftmax>;
+  static size_t attr = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return false;
+    attr = smem;
+  }
+  int64_t blocks = cdiv64(rows, kStreamWarps);
+  if (blocks > sm_count()) blocks = sm_count();
+  kern<<<(unsigned)blocks, kStreamWarps * 32, smem, s>>>(in, in_rs, w, out, out_rs, rows,
+                                                         (int)cols, (int)stages);
+  return true;
 }
 
 // ---- generic strided path -------------------------------------------------
@@ -219,8 +414,11 @@ static int run_rows(const LaunchArgs& A) {
   }
   bool fast = ics == 1 && ocs == 1 && C == OC && cp >= C && (softmax || (ws == 1 && wn == C));
   if (fast) {
-    bool ok = softmax ? try_vec<T, true>(in, irs, nullptr, out, ors, R, C, A.stream)
-                      : try_vec<T, false>(in, irs, w, out, ors, R, C, A.stream);
+    bool ok = softmax ? try_stream<T, true>(in, irs, nullptr, out, ors, R, C, A.stream)
+                      : try_stream<T, false>(in, irs, w, out, ors, R, C, A.stream);
+    if (ok) return check_launch("rowwise stream", NTB_PATH_ROW_STREAM);
+    ok = softmax ? try_vec<T, true>(in, irs, nullptr, out, ors, R, C, A.stream)
+                 : try_vec<T, false>(in, irs, w, out, ors, R, C, A.stream);
     if (ok) return check_launch("rowwise vec", NTB_PATH_ROW_VEC);
   }
   int threads = 256;
