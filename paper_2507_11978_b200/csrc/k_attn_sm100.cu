@@ -1,6 +1,367 @@
-// placeholder until the tcgen05 attention kernel lands
+// scaled_dot_product_attention on the sm_100a tensor cores (builder-defined
+// spec: the reference declares sdpa out of scope, catalog.py:36; the paper's
+// sdpa is FlashAttention-2).
+//
+// One CTA per (batch, head, 128 query rows); KV streamed in 128-row tiles:
+//   * warp 0: TMA producer - Q once, then K_j / V_j into a 2-stage ring
+//     (128B-swizzled; K K-major, V MN-major as the B operand of P.V);
+//   * warp 1: one thread issues tcgen05.mma: S_j = Q K_j^T into one of two
+//     TMEM S buffers (128 x 128 fp32), then O += P_j V_j into the TMEM O
+//     accumulator (128 x D fp32); S_{j+1} is issued before P_j is ready so
+//     the tensor core overlaps the softmax of the previous tile;
+//   * warps 4-7: softmax, ONE THREAD PER QUERY ROW (the 32x32b TMEM load
+//     hands each thread its own row, so row max / row sum need no shuffles);
+//     exp2 with the 1/sqrt(D)*log2(e) scale folded in; P written as fp16
+//     into a double-buffered 128B-swizzled smem tile (the A operand of
+//     P.V); lazy rescaling: the running max used for P only moves when a
+//     row max grows by more than 2^8, and only then is the O row (TMEM)
+//     rescaled - the final O / l uses the same max, so the result is exact
+//     softmax attention.
+// Keys beyond S_k are masked to -inf in the last tile; query rows beyond S_q
+// are computed but not stored.
+// Tensor roofline: 4*B*H*S_q*S_k*D flop per launch.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "k_sm100.cuh"
+#include "sm100_ptx.cuh"
+
 namespace ntb {
-int attn_sm100(const AttnDesc&, int, cudaStream_t) { return NTB_ERR_UNSUPPORTED; }
+namespace {
+
+constexpr int BM = 128, BN = 128;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct AttnMaps {
+  CUtensorMap q, k, v;
+};
+
+struct AttnParams {
+  int B, H, Sq, Sk;
+  float scale_log2;
+  void* o;
+  int64_t os[4];
+};
+
+template <int D>
+struct Layout {
+  static constexpr int DCH = D / 64;              // 128B chunks along D
+  static constexpr int Q_BYTES = BM * D * 2;
+  static constexpr int K_BYTES = BN * D * 2;
+  static constexpr int V_BYTES = BN * D * 2;
+  static constexpr int KV_BYTES = K_BYTES + V_BYTES;
+  static constexpr int P_BYTES = BM * BN * 2;      // 2 chunks of 64 keys
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_KV = Q_BYTES;
+  static constexpr int OFF_P = OFF_KV + 2 * KV_BYTES;
+  static constexpr int SMEM = OFF_P + 2 * P_BYTES + 1024;
+};
+
+template <bool BF16>
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  return BF16 ? sm100::pack_bf16(a, b) : sm100::pack_f16(a, b);
+}
+
+template <int D, bool BF16>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_kernel(const __grid_constant__ AttnMaps maps, const AttnParams p) {
+  using namespace sm100;
+  using L = Layout<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2],
+      p_full[2], p_free[2], pv_done;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int n_kv = (p.Sk + BN - 1) / BN;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&q_full, 1);
+    mbar_init(&pv_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_free[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(&tmem_slot, 512);
+    tc_fence_before();
+  }
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const uint32_t t_s0 = tmem, t_o = tmem + 2 * BN;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch(&maps.q);
+      tma_prefetch(&maps.k);
+      tma_prefetch(&maps.v);
+      mbar_expect_tx(&q_full, L::Q_BYTES);
+#pragma unroll
+      for (int c = 0; c < L::DCH; ++c)
+        tma_load_4d(smem + L::OFF_Q + c * (BM * 128), &maps.q, &q_full, c * 64, qt * BM, h, b);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&kv_empty[st], ph ^ 1);
+        mbar_expect_tx(&kv_full[st], L::KV_BYTES);
+        uint8_t* kdst = smem + L::OFF_KV + st * L::KV_BYTES;
+        uint8_t* vdst = kdst + L::K_BYTES;
+#pragma unroll
+        for (int c = 0; c < L::DCH; ++c) {
+          tma_load_4d(kdst + c * (BN * 128), &maps.k, &kv_full[st], c * 64, j * BN, h, b);
+          tma_load_4d(vdst + c * (BN * 128), &maps.v, &kv_full[st], c * 64, j * BN, h, b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = idesc_f16(BF16, false, false, BM, BN);
+      constexpr uint32_t idesc_o = idesc_f16(BF16, false, true, BM, D);
+      const uint32_t q_addr = smem_u32(smem + L::OFF_Q);
+      mbar_wait(&q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(&s_free[st], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(smem + L::OFF_KV + st * L::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+          const uint32_t koff = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
+          mma_f16_ss(t_s0 + st * BN, umma_desc_sw128(q_addr + off, 16, 1024),
+                     umma_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk != 0);
+        }
+        mma_commit(&s_full[st]);
+      };
+      issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        if (j + 1 < n_kv) issue_s(j + 1);
+        mbar_wait(&p_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(smem + L::OFF_KV + st * L::KV_BYTES + L::K_BYTES);
+        const uint32_t p_addr = smem_u32(smem + L::OFF_P + st * L::P_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint32_t poff = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
+          mma_f16_ss(t_o, umma_desc_sw128(p_addr + poff, 16, 1024),
+                     umma_desc_sw128(v_addr + kk * 2048, BN * 128, 1024), idesc_o,
+                     (j | kk) != 0);
+        }
+        mma_commit(&kv_empty[st]);
+        mma_commit(&p_free[st]);
+        mma_commit(&pv_done);
+      }
+    }
+  } else if (warp >= 4) {
+    const int quad = warp - 4;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_s = t_s0 + st * BN + lane_off;
+      const int kvalid = p.Sk - j * BN;  // keys of this tile that exist
+      // pass 1: row max of the raw scores
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_s + c * 32, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i < kvalid) mx = fmaxf(mx, __uint_as_float(v[i]));
+      }
+      const float cand = mx * p.scale_log2;
+      const bool grow = cand > m_used + kRescaleThreshold;
+      const bool warp_grow = __any_sync(0xffffffffu, grow);
+      float alpha = 1.f;
+      float m_new = m_used;
+      if (warp_grow) {
+        m_new = fmaxf(m_used, cand);
+        alpha = exp2f(m_used - m_new);
+      }
+      // P buffer st must be free (PV_{j-2} done)
+      mbar_wait(&p_free[st], ((j >> 1) & 1) ^ 1);
+      // pass 2: P = exp2(s*scale - m) -> fp16 smem (swizzled K-major), row sum
+      uint8_t* pbuf = smem + L::OFF_P + st * L::P_BYTES;
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_s + c * 32, v);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float e0 = (c * 32 + i < kvalid) ? exp2f(fmaf(__uint_as_float(v[i]), p.scale_log2, -m_new)) : 0.f;
+          float e1 = (c * 32 + i + 1 < kvalid) ? exp2f(fmaf(__uint_as_float(v[i + 1]), p.scale_log2, -m_new)) : 0.f;
+          sum += e0 + e1;
+          pk[i / 2] = pack2<BF16>(e0, e1);
+        }
+        // 32 keys = 4 units of 16 B in chunk (c / 2), unit base (c & 1) * 4
+        uint8_t* chunk = pbuf + (c >> 1) * (BM * 128) + row * 128;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int unit = ((c & 1) * 4 + u) ^ (row & 7);
+          *reinterpret_cast<uint4*>(chunk + unit * 16) =
+              make_uint4(pk[u * 4], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
+        }
+      }
+      l = l * alpha + sum;
+      // S buffer may be reused by S_{j+2}
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[st]);
+      // rescale the O row when this warp's running max moved (PV_{j-1} must be done)
+      if (warp_grow && j > 0) {
+        mbar_wait(&pv_done, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+          tmem_st_32x32b_x32(t_o + lane_off + c * 32, v);
+        }
+        tmem_st_wait();
+      }
+      m_used = m_new;
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[st]);
+    }
+    // epilogue: O / l -> global
+    mbar_wait(&pv_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const int qrow = qt * BM + row;
+    const float inv = 1.f / l;
+    char* obase = reinterpret_cast<char*>(p.o) +
+                  ((int64_t)b * p.os[0] + (int64_t)h * p.os[1] + (int64_t)qrow * p.os[2]) * 2;
+    const bool vec = p.os[3] == 1 && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0);
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+      tmem_ld_wait();
+      if (qrow < p.Sq) {
+        if (vec) {
+          uint4* dst = reinterpret_cast<uint4*>(obase + c * 64);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              w[e] = pack2<BF16>(__uint_as_float(v[u * 8 + e * 2]) * inv,
+                                 __uint_as_float(v[u * 8 + e * 2 + 1]) * inv);
+            dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float f = __uint_as_float(v[i]) * inv;
+            const int64_t off = (int64_t)(c * 32 + i) * p.os[3] * 2;
+            if constexpr (BF16)
+              *reinterpret_cast<__nv_bfloat16*>(obase + off) = __float2bfloat16_rn(f);
+            else
+              *reinterpret_cast<__half*>(obase + off) = __float2half_rn(f);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D, bool BF16>
+int launch_attn(const AttnMaps& maps, const AttnParams& p, cudaStream_t s) {
+  using L = Layout<D>;
+  auto k = attn_fwd_kernel<D, BF16>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+    if (e != cudaSuccess) return cuda_fail(e, "attention smem attribute");
+    attr_set = true;
+  }
+  dim3 grid((unsigned)((p.Sq + BM - 1) / BM), (unsigned)p.H, (unsigned)p.B);
+  k<<<grid, 256, L::SMEM, s>>>(maps, p);
+  return check_launch("sdpa tcgen05", NTB_PATH_ATTN_TC);
+}
+
+bool map4(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int64_t D, int64_t S, int64_t H,
+          int64_t B, const int64_t* st, uint32_t rows) {
+  if (st[3] != 1) return false;
+  for (int i = 0; i < 3; ++i)
+    if ((st[i] * 2) % 16 || st[i] <= 0) return false;
+  uint64_t dims[4] = {(uint64_t)D, (uint64_t)S, (uint64_t)H, (uint64_t)B};
+  uint64_t str[3] = {(uint64_t)st[2] * 2, (uint64_t)st[1] * 2, (uint64_t)st[0] * 2};
+  uint32_t box[4] = {64, rows, 1, 1};
+  return encode_tmap(m, dt, 4, base, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+}  // namespace
+
+int attn_sm100(const AttnDesc& a, int dtype, cudaStream_t s) {
+  if (a.D != 64 && a.D != 128) return NTB_ERR_UNSUPPORTED;
+  if (a.Sk < 1 || a.Sq < 1 || a.B >= 65536 || a.H >= 65536 || a.Sq >= (1 << 30) ||
+      a.Sk >= (1 << 30))
+    return NTB_ERR_UNSUPPORTED;
+  if (!aligned16(a.q) || !aligned16(a.k) || !aligned16(a.v)) return NTB_ERR_UNSUPPORTED;
+  const bool bf16 = dtype == NTB_BF16;
+  const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  int64_t qs[4], ks[4], vs[4];
+  for (int i = 0; i < 4; ++i) {
+    qs[i] = a.qs[i];
+    ks[i] = a.ks[i];
+    vs[i] = a.vs[i];
+  }
+  // size-1 dims: any stride is fine for TMA but must still be a 16B multiple
+  auto fix = [](int64_t* st, int64_t B, int64_t H, int64_t S, int64_t D) {
+    if (B == 1) st[0] = H * S * D;
+    if (H == 1) st[1] = S * D;
+    if (S == 1) st[2] = D;
+  };
+  fix(qs, a.B, a.H, a.Sq, a.D);
+  fix(ks, a.B, a.H, a.Sk, a.D);
+  fix(vs, a.B, a.H, a.Sk, a.D);
+  AttnMaps maps;
+  if (!map4(&maps.q, dt, a.q, a.D, a.Sq, a.H, a.B, qs, BM) ||
+      !map4(&maps.k, dt, a.k, a.D, a.Sk, a.H, a.B, ks, BN) ||
+      !map4(&maps.v, dt, a.v, a.D, a.Sk, a.H, a.B, vs, BN))
+    return NTB_ERR_UNSUPPORTED;
+  AttnParams p;
+  p.B = (int)a.B;
+  p.H = (int)a.H;
+  p.Sq = (int)a.Sq;
+  p.Sk = (int)a.Sk;
+  p.scale_log2 = a.scale * kLog2e;
+  p.o = a.o;
+  for (int i = 0; i < 4; ++i) p.os[i] = a.os[i];
+  if (a.D == 128) return bf16 ? launch_attn<128, true>(maps, p, s) : launch_attn<128, false>(maps, p, s);
+  return bf16 ? launch_attn<64, true>(maps, p, s) : launch_attn<64, false>(maps, p, s);
+}
+
 }  // namespace ntb

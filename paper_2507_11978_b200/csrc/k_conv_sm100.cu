@@ -1,6 +1,304 @@
-// placeholder until the tcgen05 implicit-GEMM conv kernel lands
+// conv2d (NCHW, stride 1, no padding) as an implicit GEMM on the sm_100a
+// tensor cores (reference catalog.py:295-330, conv2d.py.golden; oracle.py:64-80).
+//
+// The reference lowers conv2d to the matmul arrangement over
+//   M = N*P*Q pixels, K = C*R*S, N = K_out
+// with the image addressed through mixed-radix // and % maps
+// (conv2d.py.golden:56).  On B200 the same product is computed transposed,
+//   D[k_out, pixel] = sum_{(r,s), c} W'[k_out, (r,s), c] * X[c, pixel + r*W + s]
+// where "pixel" runs over a VIRTUAL output row width of W (not Q): for a
+// fixed (r, s, c) the 256 pixels of a tile are then one contiguous run of
+// the image plane, so each 64-pixel chunk is a single TMA box of the NCHW
+// input viewed as [N][C][H*W] - an MN-major, 128B-swizzled UMMA operand,
+// no im2col buffer and no NHWC pass.  The W - Q "virtual" columns (2 of 56
+// at the BASELINE shape) are computed and discarded (96.4% useful work).
+// The filter is repacked once per call to W'[k_out][(r,s)][c] (K-major).
+//
+// Pipeline = the CTA-pair GEMM of k_gemm_sm100.cu: 2-SM clusters, tile
+// 256 (k_out) x 256 (pixels), 6-stage TMA ring, tcgen05.mma.cta_group::2,
+// double-buffered TMEM accumulators, and an epilogue that transposes each
+// 32x32 accumulator block through shared memory so that a warp's stores run
+// along the output rows (coalesced NCHW writes).
+// Tensor roofline: 2*N*P*Q*K*C*R*S flop per launch.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "k_sm100.cuh"
+#include "sm100_ptx.cuh"
+
 namespace ntb {
-int conv_sm100(const ConvDesc&, int, cudaStream_t) { return NTB_ERR_UNSUPPORTED; }
+namespace {
+
+constexpr int BK = 64;
+constexpr int STAGES = 6;
+constexpr int A_BYTES = 128 * BK * 2;
+constexpr int B_BYTES = 128 * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int XPOSE_FLOATS = 32 * 33;                       // per epilogue warp
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4 * XPOSE_FLOATS * 4 + 1024;
+constexpr int TMEM_COLS = 512;
+
+struct ConvMaps {
+  CUtensorMap w;  // W' dims {C8, RS, K}
+  CUtensorMap x;  // X dims {H*W, C, N}
+};
+
+struct ConvParams {
+  int N, C, H, W, K, R, S, P, Q;
+  int cb;            // channel blocks of 64
+  int pix_tiles;     // per image: cdiv(P*W, 256)
+  int k_tiles;       // cdiv(K, 256)
+  void* y;
+  int64_t ys[4];
+};
+
+// W'[k][rs][c8] <- W[k][c][r][s] (zero for c >= C)
+template <typename T>
+__global__ void repack_filter(const T* __restrict__ w, int64_t s0, int64_t s1, int64_t s2,
+                              int64_t s3, T* __restrict__ out, int K, int C, int C8, int R,
+                              int S) {
+  const int64_t total = (int64_t)K * R * S * C8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C8);
+    const int64_t rest = i / C8;
+    const int rs = (int)(rest % (R * S));
+    const int k = (int)(rest / (R * S));
+    const int r = rs / S, s = rs % S;
+    out[i] = c < C ? w[k * s0 + c * s1 + r * s2 + s * s3] : T(0.f);
+  }
+}
+
+template <bool BF16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    conv_pair_kernel(const __grid_constant__ ConvMaps maps, const ConvParams p) {
+  using namespace sm100;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  float* xpose = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int RS = p.R * p.S;
+  const int nk = RS * p.cb;
+  const int tiles_img = p.pix_tiles * p.k_tiles;
+  const int total = tiles_img * p.N;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&maps.w);
+    tma_prefetch(&maps.x);
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(&tmem_slot, TMEM_COLS);
+    tc_fence_before();
+  }
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int t = cid; t < total; t += ncl) {
+        const int n = t / tiles_img, rr = t % tiles_img;
+        const int pt = rr / p.k_tiles, kt = rr % p.k_tiles;
+        const int krow = kt * 256 + (int)rank * 128;
+        const int pix = pt * 256 + (int)rank * 128;
+        for (int kb = 0; kb < nk; ++kb) {
+          const int rs = kb / p.cb, cbk = kb % p.cb;
+          const int shift = (rs / p.S) * p.W + (rs % p.S);
+          mbar_wait(&empty[st], ph ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[st], 2 * STAGE_BYTES);
+          const uint32_t bar = leader_addr(&full[st]);
+          tma_load_3d_pair(sA + st * A_BYTES, &maps.w, bar, cbk * BK, rs, krow);
+          uint8_t* b_dst = sB + st * B_BYTES;
+          tma_load_3d_pair(b_dst, &maps.x, bar, pix + shift, cbk * BK, n);
+          tma_load_3d_pair(b_dst + BK * 128, &maps.x, bar, pix + 64 + shift, cbk * BK, n);
+          if (++st == STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && elect_one()) {
+      constexpr uint32_t idesc = idesc_f16(BF16, false, true, 256, 256);
+      int st = 0;
+      uint32_t ph = 0;
+      int tl = 0;
+      for (int t = cid; t < total; t += ncl, ++tl) {
+        const int acc = tl & 1;
+        const uint32_t aph = (tl >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + st * A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + st * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024);
+            mma_f16_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit_pair(&empty[st]);
+          if (++st == STAGES) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    float* xp = xpose + ew * XPOSE_FLOATS;
+    const int PW = p.P * p.W;
+    int tl = 0;
+    for (int t = cid; t < total; t += ncl, ++tl) {
+      const int n = t / tiles_img, rr = t % tiles_img;
+      const int pt = rr / p.k_tiles, kt = rr % p.k_tiles;
+      const int acc = tl & 1;
+      const uint32_t aph = (tl >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int k0 = kt * 256 + (int)rank * 128 + ew * 32;  // this warp's 32 output channels
+      const uint32_t taddr = tmem_base + acc * 256 + ((uint32_t)(ew * 32) << 16);
+      char* ybase = reinterpret_cast<char*>(p.y) + (int64_t)n * p.ys[0] * 2;
+#pragma unroll 1
+      for (int cc = 0; cc < 8; ++cc) {
+        uint32_t v[32];
+        __syncwarp();
+        tmem_ld_32x32b_x32(taddr + cc * 32, v);
+        tmem_ld_wait();
+        // lane = output channel row; transpose so lanes run along pixels
+#pragma unroll
+        for (int i = 0; i < 32; ++i) xp[lane * 33 + i] = __uint_as_float(v[i]);
+        __syncwarp();
+        const int m = pt * 256 + cc * 32 + lane;  // virtual pixel of this lane
+        const int pp = m / p.W, q = m - pp * p.W;
+        const bool ok = m < PW && q < p.Q;
+        const int64_t pix_off = (int64_t)pp * p.ys[2] + (int64_t)q * p.ys[3];
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+          const int k = k0 + j;
+          if (ok && k < p.K) {
+            const float f = xp[j * 33 + lane];
+            const int64_t off = (int64_t)k * p.ys[1] + pix_off;
+            if constexpr (BF16)
+              reinterpret_cast<__nv_bfloat16*>(ybase)[off] = __float2bfloat16_rn(f);
+            else
+              reinterpret_cast<__half*>(ybase)[off] = __float2half_rn(f);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+    }
+  }
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, TMEM_COLS);
+  }
+}
+
+template <bool BF16>
+int launch_conv(const ConvMaps& maps, const ConvParams& p, cudaStream_t s) {
+  auto k = conv_pair_kernel<BF16>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "conv smem attribute");
+    attr_set = true;
+  }
+  const int total = p.N * p.pix_tiles * p.k_tiles;
+  int clusters = sm_count() / 2;
+  if (total < clusters) clusters = total;
+  k<<<2 * clusters, 256, SMEM_BYTES, s>>>(maps, p);
+  return check_launch("conv2d tcgen05 pair", NTB_PATH_CONV_TC);
+}
+
+}  // namespace
+
+int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
+  // TMA view of the image as [N][C][H*W]: contiguous planes, 16B-aligned strides
+  if (c.xs[3] != 1 || c.xs[2] != c.W) return NTB_ERR_UNSUPPORTED;
+  if ((c.xs[1] * 2) % 16 || (c.N > 1 && (c.xs[0] * 2) % 16) || !aligned16(c.x))
+    return NTB_ERR_UNSUPPORTED;
+  if (c.N >= 65536 || c.K >= (1 << 30) || (int64_t)c.H * c.W >= (1ll << 31) || c.C >= (1 << 30))
+    return NTB_ERR_UNSUPPORTED;
+  const bool bf16 = dtype == NTB_BF16;
+  const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const int64_t C8 = (c.C + 7) / 8 * 8;
+  const int64_t RS = c.R * c.S;
+  const size_t wbytes = (size_t)c.K * RS * C8 * 2;
+  void* wp = workspace(wbytes, s);
+  if (!wp) return fail(NTB_ERR_CUDA, "conv2d: workspace allocation failed");
+  {
+    int64_t total = c.K * RS * C8;
+    int blocks = (int)cdiv64(total, 256);
+    if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+    if (bf16)
+      repack_filter<__nv_bfloat16><<<blocks, 256, 0, s>>>(
+          (const __nv_bfloat16*)c.w, c.ws[0], c.ws[1], c.ws[2], c.ws[3], (__nv_bfloat16*)wp,
+          (int)c.K, (int)c.C, (int)C8, (int)c.R, (int)c.S);
+    else
+      repack_filter<__half><<<blocks, 256, 0, s>>>((const __half*)c.w, c.ws[0], c.ws[1], c.ws[2],
+                                                   c.ws[3], (__half*)wp, (int)c.K, (int)c.C,
+                                                   (int)C8, (int)c.R, (int)c.S);
+    int rc = check_launch("conv2d filter repack", NTB_PATH_REPACK);
+    if (rc) return rc;
+  }
+  ConvMaps maps;
+  {
+    uint64_t dims[3] = {(uint64_t)C8, (uint64_t)RS, (uint64_t)c.K};
+    uint64_t str[2] = {(uint64_t)C8 * 2, (uint64_t)(RS * C8 * 2)};
+    uint32_t box[3] = {64, 1, 128};
+    if (!encode_tmap(&maps.w, dt, 3, wp, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return fail(NTB_ERR_UNSUPPORTED, "conv2d: filter tensor map");
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)(c.H * c.W), (uint64_t)c.C, (uint64_t)c.N};
+    uint64_t str[2] = {(uint64_t)c.xs[1] * 2,
+                       c.N > 1 ? (uint64_t)c.xs[0] * 2 : (uint64_t)c.xs[1] * 2 * c.C};
+    uint32_t box[3] = {64, 64, 1};
+    if (!encode_tmap(&maps.x, dt, 3, c.x, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return fail(NTB_ERR_UNSUPPORTED, "conv2d: image tensor map");
+  }
+  ConvParams p;
+  p.N = (int)c.N; p.C = (int)c.C; p.H = (int)c.H; p.W = (int)c.W; p.K = (int)c.K;
+  p.R = (int)c.R; p.S = (int)c.S; p.P = (int)c.P; p.Q = (int)c.Q;
+  p.cb = (int)cdiv64(c.C, BK);
+  p.pix_tiles = (int)cdiv64((int64_t)c.P * c.W, 256);
+  p.k_tiles = (int)cdiv64(c.K, 256);
+  p.y = c.y;
+  for (int d = 0; d < 4; ++d) p.ys[d] = c.ys[d];
+  return bf16 ? launch_conv<true>(maps, p, s) : launch_conv<false>(maps, p, s);
+}
+
 }  // namespace ntb

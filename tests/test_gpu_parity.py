@@ -235,7 +235,10 @@ def test_conv2d_half(dtype, shape):
     x = _r16(rng.uniform(-1, 1, (n, c, h, w)).astype(np.float32), dtype)
     f = _r16(rng.uniform(-1, 1, (k, c, r, s)).astype(np.float32), dtype)
     meta = {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128, "BLOCK_SIZE_K": 64}
-    got = _run("conv2d", {"input": x, "filter": f}, meta, dtype)
+    with _Paths() as pc:
+        got = _run("conv2d", {"input": x, "filter": f}, meta, dtype)
+    if (h * w) % 8 == 0:
+        assert pc.delta["conv_tc"] == 1
     _close(got, oracle.conv2d(x, f), rtol=1e-2, atol=3e-2)
 
 
@@ -247,9 +250,11 @@ def test_sdpa_half(dtype, bhsd):
     rng = np.random.default_rng(s)
     q, k, v = (_r16(rng.uniform(-1, 1, (b, h, s, d)).astype(np.float32), dtype)
                for _ in range(3))
-    got = _run("sdpa", {"q": q, "k": k, "v": v, "o": None},
-               {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128}, dtype,
-               out=torch.zeros((b, h, s, d), device=DEV, dtype=dtype))
+    with _Paths() as pc:
+        got = _run("sdpa", {"q": q, "k": k, "v": v, "o": None},
+                   {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128}, dtype,
+                   out=torch.zeros((b, h, s, d), device=DEV, dtype=dtype))
+    assert pc.delta["attn_tc"] == 1
     _close(got, oracle.sdpa(q, k, v), rtol=1e-2, atol=1e-2)
 
 
