@@ -7,12 +7,17 @@
 // (conv2d.py.golden:56).  On B200 the same product is computed transposed,
 //   D[k_out, pixel] = sum_{(r,s), c} W'[k_out, (r,s), c] * X[c, pixel + r*W + s]
 // where "pixel" runs over a VIRTUAL output row width of W (not Q): for a
-// fixed (r, s, c) the 256 pixels of a tile are then one contiguous run of
-// the image plane, so each 64-pixel chunk is a single TMA box of the NCHW
-// input viewed as [N][C][H*W] - an MN-major, 128B-swizzled UMMA operand,
-// no im2col buffer and no NHWC pass.  The W - Q "virtual" columns (2 of 56
-// at the BASELINE shape) are computed and discarded (96.4% useful work).
-// The filter is repacked once per call to W'[k_out][(r,s)][c] (K-major).
+// fixed (r, s) the 256 pixels of a tile then read one contiguous run of
+// image pixels starting at pixel + r*W + s, i.e. a plain 2-D TMA box of the
+// image viewed as [N][H*W][C] (channels innermost, K-major operand) - no
+// im2col buffer.  The W - Q "virtual" columns (2 of 56 at the BASELINE
+// shape) are computed and discarded (96.4% useful work).
+// TMA needs the innermost box coordinate 16-byte aligned, so the (r, s)
+// shift must fall on the pixel dimension, not the innermost one: NCHW
+// inputs are therefore transposed once per call to [N][H*W][C8] (C padded
+// to a multiple of 8) by a tiled smem transpose (2 x image bytes of HBM
+// traffic); channels_last inputs are consumed in place.  The filter is
+// repacked to W'[k_out][(r,s)][C8] (K-major).
 //
 // Pipeline = the CTA-pair GEMM of k_gemm_sm100.cu: 2-SM clusters, tile
 // 256 (k_out) x 256 (pixels), 6-stage TMA ring, tcgen05.mma.cta_group::2,
@@ -41,7 +46,7 @@ constexpr int TMEM_COLS = 512;
 
 struct ConvMaps {
   CUtensorMap w;  // W' dims {C8, RS, K}
-  CUtensorMap x;  // X dims {H*W, C, N}
+  CUtensorMap x;  // X' dims {C8, H*W, N} (channels innermost)
 };
 
 struct ConvParams {
@@ -67,6 +72,29 @@ __global__ void repack_filter(const T* __restrict__ w, int64_t s0, int64_t s1, i
     const int k = (int)(rest / (R * S));
     const int r = rs / S, s = rs % S;
     out[i] = c < C ? w[k * s0 + c * s1 + r * s2 + s * s3] : T(0.f);
+  }
+}
+
+// X'[n][pix][c8] <- X[n][c][pix] through a 64x64 smem tile (coalesced both ways)
+template <typename T>
+__global__ void __launch_bounds__(256) nchw_to_nhwc(const T* __restrict__ x, int64_t sn,
+                                                    int64_t sc, T* __restrict__ out, int C,
+                                                    int C8, int HW) {
+  __shared__ T tile[64][66];
+  const int n = blockIdx.z;
+  const int c0 = blockIdx.y * 64, p0 = blockIdx.x * 64;
+  const T* src = x + (int64_t)n * sn;
+  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
+    const int cc = i / 64, pp = i % 64;
+    const int c = c0 + cc, pix = p0 + pp;
+    tile[cc][pp] = (c < C && pix < HW) ? src[(int64_t)c * sc + pix] : T(0.f);
+  }
+  __syncthreads();
+  T* dst = out + (int64_t)n * HW * C8;
+  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
+    const int pp = i / 64, cc = i % 64;
+    const int c = c0 + cc, pix = p0 + pp;
+    if (c < C8 && pix < HW) dst[(int64_t)pix * C8 + c] = tile[cc][pp];
   }
 }
 
@@ -130,9 +158,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           if (rank == 0) mbar_expect_tx(&full[st], 2 * STAGE_BYTES);
           const uint32_t bar = leader_addr(&full[st]);
           tma_load_3d_pair(sA + st * A_BYTES, &maps.w, bar, cbk * BK, rs, krow);
-          uint8_t* b_dst = sB + st * B_BYTES;
-          tma_load_3d_pair(b_dst, &maps.x, bar, pix + shift, cbk * BK, n);
-          tma_load_3d_pair(b_dst + BK * 128, &maps.x, bar, pix + 64 + shift, cbk * BK, n);
+          tma_load_3d_pair(sB + st * B_BYTES, &maps.x, bar, cbk * BK, pix + shift, n);
           if (++st == STAGES) {
             st = 0;
             ph ^= 1;
@@ -142,7 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     if (rank == 0 && elect_one()) {
-      constexpr uint32_t idesc = idesc_f16(BF16, false, true, 256, 256);
+      constexpr uint32_t idesc = idesc_f16(BF16, false, false, 256, 256);
       int st = 0;
       uint32_t ph = 0;
       int tl = 0;
@@ -160,7 +186,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = umma_desc_sw128(a_addr + k * 32, 16, 1024);
-            const uint64_t bd = umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024);
+            const uint64_t bd = umma_desc_sw128(b_addr + k * 32, 16, 1024);
             mma_f16_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
           mma_commit_pair(&empty[st]);
@@ -246,23 +272,27 @@ int launch_conv(const ConvMaps& maps, const ConvParams& p, cudaStream_t s) {
 }  // namespace
 
 int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
-  // TMA view of the image as [N][C][H*W]: contiguous planes, 16B-aligned strides
-  if (c.xs[3] != 1 || c.xs[2] != c.W) return NTB_ERR_UNSUPPORTED;
-  if ((c.xs[1] * 2) % 16 || (c.N > 1 && (c.xs[0] * 2) % 16) || !aligned16(c.x))
-    return NTB_ERR_UNSUPPORTED;
   if (c.N >= 65536 || c.K >= (1 << 30) || (int64_t)c.H * c.W >= (1ll << 31) || c.C >= (1 << 30))
     return NTB_ERR_UNSUPPORTED;
   const bool bf16 = dtype == NTB_BF16;
   const CUtensorMapDataType dt = bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  const int64_t C8 = (c.C + 7) / 8 * 8;
+  const int64_t HW = c.H * c.W;
+  // channels_last input already is [N][H][W][C]: use it in place
+  const bool nhwc = c.xs[1] == 1 && c.xs[3] == c.C && c.xs[2] == c.W * c.C &&
+                    (c.N == 1 || c.xs[0] == HW * c.C) && c.C % 8 == 0 && aligned16(c.x);
+  const int64_t C8 = nhwc ? c.C : (c.C + 7) / 8 * 8;
   const int64_t RS = c.R * c.S;
-  const size_t wbytes = (size_t)c.K * RS * C8 * 2;
-  void* wp = workspace(wbytes, s);
-  if (!wp) return fail(NTB_ERR_CUDA, "conv2d: workspace allocation failed");
+  const size_t wbytes = ((size_t)c.K * RS * C8 * 2 + 255) / 256 * 256;
+  const size_t xbytes = nhwc ? 0 : (size_t)c.N * HW * C8 * 2;
+  char* ws = (char*)workspace(wbytes + xbytes, s);
+  if (!ws) return fail(NTB_ERR_CUDA, "conv2d: workspace allocation failed");
+  void* wp = ws;
+  const void* xp = nhwc ? c.x : (const void*)(ws + wbytes);
+  const int sms = sm_count();
   {
     int64_t total = c.K * RS * C8;
     int blocks = (int)cdiv64(total, 256);
-    if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+    if (blocks > sms * 8) blocks = sms * 8;
     if (bf16)
       repack_filter<__nv_bfloat16><<<blocks, 256, 0, s>>>(
           (const __nv_bfloat16*)c.w, c.ws[0], c.ws[1], c.ws[2], c.ws[3], (__nv_bfloat16*)wp,
@@ -274,6 +304,20 @@ int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
     int rc = check_launch("conv2d filter repack", NTB_PATH_REPACK);
     if (rc) return rc;
   }
+  if (!nhwc) {
+    // NCHW planes must be contiguous H*W runs for the transpose
+    if (c.xs[3] != 1 || c.xs[2] != c.W) return NTB_ERR_UNSUPPORTED;
+    dim3 grid((unsigned)cdiv64(HW, 64), (unsigned)cdiv64(C8, 64), (unsigned)c.N);
+    if (bf16)
+      nchw_to_nhwc<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)c.x, c.xs[0], c.xs[1],
+                                                      (__nv_bfloat16*)xp, (int)c.C, (int)C8,
+                                                      (int)HW);
+    else
+      nchw_to_nhwc<__half><<<grid, 256, 0, s>>>((const __half*)c.x, c.xs[0], c.xs[1], (__half*)xp,
+                                               (int)c.C, (int)C8, (int)HW);
+    int rc = check_launch("conv2d NCHW->NHWC", NTB_PATH_REPACK);
+    if (rc) return rc;
+  }
   ConvMaps maps;
   {
     uint64_t dims[3] = {(uint64_t)C8, (uint64_t)RS, (uint64_t)c.K};
@@ -283,11 +327,10 @@ int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
       return fail(NTB_ERR_UNSUPPORTED, "conv2d: filter tensor map");
   }
   {
-    uint64_t dims[3] = {(uint64_t)(c.H * c.W), (uint64_t)c.C, (uint64_t)c.N};
-    uint64_t str[2] = {(uint64_t)c.xs[1] * 2,
-                       c.N > 1 ? (uint64_t)c.xs[0] * 2 : (uint64_t)c.xs[1] * 2 * c.C};
-    uint32_t box[3] = {64, 64, 1};
-    if (!encode_tmap(&maps.x, dt, 3, c.x, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
+    uint64_t dims[3] = {(uint64_t)C8, (uint64_t)HW, (uint64_t)c.N};
+    uint64_t str[2] = {(uint64_t)C8 * 2, (uint64_t)(HW * C8 * 2)};
+    uint32_t box[3] = {64, 128, 1};
+    if (!encode_tmap(&maps.x, dt, 3, xp, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return fail(NTB_ERR_UNSUPPORTED, "conv2d: image tensor map");
   }
   ConvParams p;

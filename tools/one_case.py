@@ -1,0 +1,42 @@
+"""Run one small case of a family on cuda:0 (debug helper for sanitizer runs)."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2507_11978_b200 import backend as B  # noqa: E402
+
+kind = sys.argv[1]
+dev = "cuda:0"
+rng = np.random.default_rng(0)
+
+
+def T(shape):
+    return torch.from_numpy(rng.uniform(-1, 1, shape).astype(np.float32)).to(dev).half()
+
+
+if kind == "conv":
+    n, c, h, w, k, r, s = (int(x) for x in sys.argv[2:9])
+    x, f = T((n, c, h, w)), T((k, c, r, s))
+    y = torch.zeros((n, k, h - r + 1, w - s + 1), device=dev, dtype=torch.float16)
+    B.conv2d_launch(x, f, y, 128, 128, 64)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float(), f.float())
+    print("conv max err", (y.float() - ref).abs().max().item(), B.path_counts())
+elif kind == "sdpa":
+    b, h, sq, d = (int(x) for x in sys.argv[2:6])
+    q, kk, v = T((b, h, sq, d)), T((b, h, sq, d)), T((b, h, sq, d))
+    o = torch.zeros_like(q)
+    B.sdpa_launch(q, kk, v, o, 128, 128)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float(), kk.float(), v.float())
+    print("sdpa max err", (o.float() - ref).abs().max().item(), B.path_counts())
+elif kind == "mm":
+    m, n, k = (int(x) for x in sys.argv[2:5])
+    a, b = T((m, k)), T((k, n))
+    c = torch.zeros((m, n), device=dev, dtype=torch.float16)
+    B.mm_launch(a, b, c, 128, 128, 64)
+    torch.cuda.synchronize()
+    print("mm", m, n, k, "max err", (c.float() - a.float() @ b.float()).abs().max().item(),
+          {k_: v for k_, v in B.path_counts().items() if v})
