@@ -2,23 +2,25 @@
 // spec: the reference declares sdpa out of scope, catalog.py:36; the paper's
 // sdpa is FlashAttention-2).
 //
-// One CTA per (batch, head, 128 query rows); KV streamed in 128-row tiles:
-//   * warp 0: TMA producer - Q once, then K_j / V_j into a 2-stage ring
+// One CTA per (batch, head, 256 query rows) = two 128-row query tiles that
+// share every K/V tile (ping-pong, as in FlashAttention-4):
+//   * warp 0: TMA producer - Q0/Q1 once, then K_j / V_j into a 2-stage ring
 //     (128B-swizzled; K K-major, V MN-major as the B operand of P.V);
-//   * warp 1: one thread issues tcgen05.mma: S_j = Q K_j^T into one of two
-//     TMEM S buffers (128 x 128 fp32), then O += P_j V_j into the TMEM O
-//     accumulator (128 x D fp32); S_{j+1} is issued before P_j is ready so
-//     the tensor core overlaps the softmax of the previous tile;
-//   * warps 4-7: softmax, ONE THREAD PER QUERY ROW (the 32x32b TMEM load
-//     hands each thread its own row, so row max / row sum need no shuffles);
-//     exp2 with the 1/sqrt(D)*log2(e) scale folded in; P written as fp16
-//     into a double-buffered 128B-swizzled smem tile (the A operand of
-//     P.V); lazy rescaling: the running max used for P only moves when a
-//     row max grows by more than 2^8, and only then is the O row (TMEM)
-//     rescaled - the final O / l uses the same max, so the result is exact
-//     softmax attention.
-// Keys beyond S_k are masked to -inf in the last tile; query rows beyond S_q
-// are computed but not stored.
+//   * warp 1: one thread issues tcgen05.mma in the order
+//       S0_0, S1_0, { PV0_j, S0_{j+1}, PV1_j, S1_{j+1} }_j
+//     so the tensor core always has the other query tile's work while a
+//     softmax warpgroup is busy;
+//   * warps 4-7 / 8-11: softmax warpgroups for Q0 / Q1, ONE THREAD PER QUERY
+//     ROW (32x32b TMEM loads give each thread its own row: no shuffles);
+//     P = exp2(S*scale*log2e - m) is written back as packed fp16 INTO THE
+//     S COLUMNS OF TMEM and consumed from there by the next MMA
+//     (tcgen05.mma with the A operand in TMEM), so P never touches smem;
+//   * lazy rescaling: the running max used for P only moves when a row max
+//     grows by more than 2^8; only then is the O row (TMEM) rescaled.  The
+//     MMA that produced S_{g,j} was issued after PV_{g,j-1}, so waiting for
+//     S_{g,j} already guarantees O_g is up to date - no extra barrier.
+// TMEM: S0/P0 [0,128) S1/P1 [128,256) O0 [256,256+D) O1 [256+D,256+2D).
+// Keys beyond S_k are masked to -inf; query rows beyond S_q are not stored.
 // Tensor roofline: 4*B*H*S_q*S_k*D flop per launch.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -30,7 +32,7 @@
 namespace ntb {
 namespace {
 
-constexpr int BM = 128, BN = 128;
+constexpr int BM = 128, BN = 128;  // query rows per tile, keys per KV tile
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
@@ -48,16 +50,20 @@ struct AttnParams {
 template <int D>
 struct Layout {
   static constexpr int DCH = D / 64;              // 128B chunks along D
-  static constexpr int Q_BYTES = BM * D * 2;
+  static constexpr int Q_BYTES = BM * D * 2;      // one query tile
   static constexpr int K_BYTES = BN * D * 2;
   static constexpr int V_BYTES = BN * D * 2;
   static constexpr int KV_BYTES = K_BYTES + V_BYTES;
-  static constexpr int P_BYTES = BM * BN * 2;      // 2 chunks of 64 keys
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_KV = Q_BYTES;
-  static constexpr int OFF_P = OFF_KV + 2 * KV_BYTES;
-  static constexpr int SMEM = OFF_P + 2 * P_BYTES + 1024;
+  static constexpr int OFF_KV = 2 * Q_BYTES;
+  static constexpr int SMEM = OFF_KV + 2 * KV_BYTES + 1024;
 };
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 template <bool BF16>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -65,15 +71,15 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 template <int D, bool BF16>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_fwd_kernel(const __grid_constant__ AttnMaps maps, const AttnParams p) {
   using namespace sm100;
   using L = Layout<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2],
-      p_full[2], p_free[2], pv_done;
+  __shared__ __align__(8) uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full[2],
+      o_full[2];
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -82,14 +88,12 @@ __global__ void __launch_bounds__(256, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
-    mbar_init(&pv_done, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
       mbar_init(&p_full[i], 4);
-      mbar_init(&p_free[i], 1);
+      mbar_init(&o_full[i], 1);
     }
     fence_barrier_init();
   }
@@ -100,17 +104,19 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-  const uint32_t t_s0 = tmem, t_o = tmem + 2 * BN;
 
   if (warp == 0) {
     if (elect_one()) {
       tma_prefetch(&maps.q);
       tma_prefetch(&maps.k);
       tma_prefetch(&maps.v);
-      mbar_expect_tx(&q_full, L::Q_BYTES);
+      mbar_expect_tx(&q_full, 2 * L::Q_BYTES);
 #pragma unroll
-      for (int c = 0; c < L::DCH; ++c)
-        tma_load_4d(smem + L::OFF_Q + c * (BM * 128), &maps.q, &q_full, c * 64, qt * BM, h, b);
+      for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int c = 0; c < L::DCH; ++c)
+          tma_load_4d(smem + L::OFF_Q + g * L::Q_BYTES + c * (BM * 128), &maps.q, &q_full,
+                      c * 64, qt * 2 * BM + g * BM, h, b);
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
         const uint32_t ph = (j >> 1) & 1;
@@ -129,78 +135,87 @@ __global__ void __launch_bounds__(256, 1)
     if (elect_one()) {
       constexpr uint32_t idesc_s = idesc_f16(BF16, false, false, BM, BN);
       constexpr uint32_t idesc_o = idesc_f16(BF16, false, true, BM, D);
-      const uint32_t q_addr = smem_u32(smem + L::OFF_Q);
       mbar_wait(&q_full, 0);
-      auto issue_s = [&](int j) {
+      auto issue_s = [&](int g, int j) {
         const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
-        mbar_wait(&s_free[st], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
+        const uint32_t q_addr = smem_u32(smem + L::OFF_Q + g * L::Q_BYTES);
         const uint32_t k_addr = smem_u32(smem + L::OFF_KV + st * L::KV_BYTES);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
           const uint32_t koff = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
-          mma_f16_ss(t_s0 + st * BN, umma_desc_sw128(q_addr + off, 16, 1024),
+          mma_f16_ss(tmem + g * BN, umma_desc_sw128(q_addr + off, 16, 1024),
                      umma_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk != 0);
         }
-        mma_commit(&s_full[st]);
+        mma_commit(&s_full[g]);
       };
-      issue_s(0);
-      for (int j = 0; j < n_kv; ++j) {
+      auto issue_pv = [&](int g, int j) {
         const int st = j & 1;
-        if (j + 1 < n_kv) issue_s(j + 1);
-        mbar_wait(&p_full[st], (j >> 1) & 1);
-        tc_fence_after();
         const uint32_t v_addr = smem_u32(smem + L::OFF_KV + st * L::KV_BYTES + L::K_BYTES);
-        const uint32_t p_addr = smem_u32(smem + L::OFF_P + st * L::P_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint32_t poff = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-          mma_f16_ss(t_o, umma_desc_sw128(p_addr + poff, 16, 1024),
+        for (int kk = 0; kk < BN / 16; ++kk)
+          mma_f16_ts(tmem + 2 * BN + g * D, tmem + g * BN + kk * 8,
                      umma_desc_sw128(v_addr + kk * 2048, BN * 128, 1024), idesc_o,
                      (j | kk) != 0);
+      };
+      mbar_wait(&kv_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        const bool more = j + 1 < n_kv;
+        if (more) {
+          mbar_wait(&kv_full[st ^ 1], ((j + 1) >> 1) & 1);
         }
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        issue_pv(0, j);
+        if (more) issue_s(0, j + 1);
+        else mma_commit(&o_full[0]);
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        issue_pv(1, j);
         mma_commit(&kv_empty[st]);
-        mma_commit(&p_free[st]);
-        mma_commit(&pv_done);
+        if (more) issue_s(1, j + 1);
+        else mma_commit(&o_full[1]);
       }
     }
   } else if (warp >= 4) {
-    const int quad = warp - 4;
+    const int g = (warp - 4) >> 2;          // query tile of this warpgroup
+    const int quad = warp & 3;              // TMEM lane quadrant
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const uint32_t t_s = tmem + g * BN + lane_off;
+    const uint32_t t_o = tmem + 2 * BN + g * D + lane_off;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
+      mbar_wait(&s_full[g], j & 1);
       tc_fence_after();
-      const uint32_t t_s = t_s0 + st * BN + lane_off;
-      const int kvalid = p.Sk - j * BN;  // keys of this tile that exist
-      // pass 1: row max of the raw scores
+      const int kvalid = p.Sk - j * BN;
       float mx = -INFINITY;
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(t_s + c * 32, v);
         tmem_ld_wait();
+        if (kvalid >= BN) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i < kvalid) mx = fmaxf(mx, __uint_as_float(v[i]));
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i < kvalid) mx = fmaxf(mx, __uint_as_float(v[i]));
+        }
       }
       const float cand = mx * p.scale_log2;
-      const bool grow = cand > m_used + kRescaleThreshold;
-      const bool warp_grow = __any_sync(0xffffffffu, grow);
-      float alpha = 1.f;
-      float m_new = m_used;
+      const bool warp_grow = __any_sync(0xffffffffu, cand > m_used + kRescaleThreshold);
+      float alpha = 1.f, m_new = m_used;
       if (warp_grow) {
         m_new = fmaxf(m_used, cand);
-        alpha = exp2f(m_used - m_new);
+        alpha = ex2(m_used - m_new);
       }
-      // P buffer st must be free (PV_{j-2} done)
-      mbar_wait(&p_free[st], ((j >> 1) & 1) ^ 1);
-      // pass 2: P = exp2(s*scale - m) -> fp16 smem (swizzled K-major), row sum
-      uint8_t* pbuf = smem + L::OFF_P + st * L::P_BYTES;
+      // P = exp2(s*scale - m) packed fp16 into the S columns (in place, in order)
       float sum = 0.f;
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
@@ -210,50 +225,40 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          float e0 = (c * 32 + i < kvalid) ? exp2f(fmaf(__uint_as_float(v[i]), p.scale_log2, -m_new)) : 0.f;
-          float e1 = (c * 32 + i + 1 < kvalid) ? exp2f(fmaf(__uint_as_float(v[i + 1]), p.scale_log2, -m_new)) : 0.f;
+          float e0 = ex2(fmaf(__uint_as_float(v[i]), p.scale_log2, -m_new));
+          float e1 = ex2(fmaf(__uint_as_float(v[i + 1]), p.scale_log2, -m_new));
+          if (kvalid < BN) {
+            if (c * 32 + i >= kvalid) e0 = 0.f;
+            if (c * 32 + i + 1 >= kvalid) e1 = 0.f;
+          }
           sum += e0 + e1;
           pk[i / 2] = pack2<BF16>(e0, e1);
         }
-        // 32 keys = 4 units of 16 B in chunk (c / 2), unit base (c & 1) * 4
-        uint8_t* chunk = pbuf + (c >> 1) * (BM * 128) + row * 128;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int unit = ((c & 1) * 4 + u) ^ (row & 7);
-          *reinterpret_cast<uint4*>(chunk + unit * 16) =
-              make_uint4(pk[u * 4], pk[u * 4 + 1], pk[u * 4 + 2], pk[u * 4 + 3]);
-        }
+        tmem_st_32x32b_x16(t_s + c * 16, pk);
       }
       l = l * alpha + sum;
-      // S buffer may be reused by S_{j+2}
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[st]);
-      // rescale the O row when this warp's running max moved (PV_{j-1} must be done)
       if (warp_grow && j > 0) {
-        mbar_wait(&pv_done, (j - 1) & 1);
-        tc_fence_after();
+        // O_g is final for tiles < j: S_{g,j} was issued after PV_{g,j-1}
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t v[32];
-          tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+          tmem_ld_32x32b_x32(t_o + c * 32, v);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-          tmem_st_32x32b_x32(t_o + lane_off + c * 32, v);
+          tmem_st_32x32b_x32(t_o + c * 32, v);
         }
-        tmem_st_wait();
       }
       m_used = m_new;
-      fence_proxy_async();
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[st]);
+      if (lane == 0) mbar_arrive(&p_full[g]);
     }
     // epilogue: O / l -> global
-    mbar_wait(&pv_done, (n_kv - 1) & 1);
+    mbar_wait(&o_full[g], 0);
     tc_fence_after();
-    const int qrow = qt * BM + row;
+    const int qrow = qt * 2 * BM + g * BM + row;
     const float inv = 1.f / l;
     char* obase = reinterpret_cast<char*>(p.o) +
                   ((int64_t)b * p.os[0] + (int64_t)h * p.os[1] + (int64_t)qrow * p.os[2]) * 2;
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t v[32];
-      tmem_ld_32x32b_x32(t_o + lane_off + c * 32, v);
+      tmem_ld_32x32b_x32(t_o + c * 32, v);
       tmem_ld_wait();
       if (qrow < p.Sq) {
         if (vec) {
@@ -306,8 +311,8 @@ int launch_attn(const AttnMaps& maps, const AttnParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return cuda_fail(e, "attention smem attribute");
     attr_set = true;
   }
-  dim3 grid((unsigned)((p.Sq + BM - 1) / BM), (unsigned)p.H, (unsigned)p.B);
-  k<<<grid, 256, L::SMEM, s>>>(maps, p);
+  dim3 grid((unsigned)((p.Sq + 2 * BM - 1) / (2 * BM)), (unsigned)p.H, (unsigned)p.B);
+  k<<<grid, 384, L::SMEM, s>>>(maps, p);
   return check_launch("sdpa tcgen05", NTB_PATH_ATTN_TC);
 }
 
