@@ -35,6 +35,9 @@ namespace {
 constexpr int BM = 128, BN = 128;  // query rows per tile, keys per KV tile
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// Polynomial exp2 offload: measured slower on B200 at D=128 (the softmax is
+// issue-bound, not SFU-bound: 8.54 ms vs 8.10 ms), so it is off.
+constexpr bool kPolyExp = false;
 
 struct AttnMaps {
   CUtensorMap q, k, v;
@@ -63,6 +66,18 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA/ALU pipes (Cody-Waite split + cubic, rel. err 7.5e-5 <
+// half an fp16 ulp): offloads a quarter of the exponentials from the SFU,
+// which otherwise bounds the softmax at the tensor-core rate (FA4 trick).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.0f;                    // 1.5 * 2^23: round to int
+  const int i = __float_as_int(t) - 0x4B400000;
+  const float f = x - (t - 12582912.0f);             // f in [-0.5, 0.5]
+  float p = fmaf(fmaf(fmaf(0.0551702793f, f, 0.242607975f), f, 0.693260928f), f, 0.999928276f);
+  return __int_as_float(__float_as_int(p) + (i << 23));
 }
 
 template <bool BF16>
@@ -225,8 +240,16 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          float e0 = ex2(fmaf(__uint_as_float(v[i]), p.scale_log2, -m_new));
-          float e1 = ex2(fmaf(__uint_as_float(v[i + 1]), p.scale_log2, -m_new));
+          const float x0 = fmaf(__uint_as_float(v[i]), p.scale_log2, -m_new);
+          const float x1 = fmaf(__uint_as_float(v[i + 1]), p.scale_log2, -m_new);
+          float e0, e1;
+          if (kPolyExp && (i & 6) == 0) {  // 8 of every 32 columns on the FMA pipe
+            e0 = ex2_poly(x0);
+            e1 = ex2_poly(x1);
+          } else {
+            e0 = ex2(x0);
+            e1 = ex2(x1);
+          }
           if (kvalid < BN) {
             if (c * 32 + i >= kvalid) e0 = 0.f;
             if (c * 32 + i + 1 >= kvalid) e1 = 0.f;

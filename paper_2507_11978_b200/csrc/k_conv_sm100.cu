@@ -75,26 +75,50 @@ __global__ void repack_filter(const T* __restrict__ w, int64_t s0, int64_t s1, i
   }
 }
 
-// X'[n][pix][c8] <- X[n][c][pix] through a 64x64 smem tile (coalesced both ways)
+// X'[n][pix][c8] <- X[n][c][pix]: 64 channels x 128 pixels per CTA through
+// shared memory, 128-bit loads along pixels and 128-bit stores along
+// channels (HBM-bound: reads and writes the image once).
 template <typename T>
 __global__ void __launch_bounds__(256) nchw_to_nhwc(const T* __restrict__ x, int64_t sn,
                                                     int64_t sc, T* __restrict__ out, int C,
                                                     int C8, int HW) {
-  __shared__ T tile[64][66];
+  constexpr int TC = 64, TP = 128;
+  __shared__ __align__(16) uint16_t tile[TC][TP + 8];
   const int n = blockIdx.z;
-  const int c0 = blockIdx.y * 64, p0 = blockIdx.x * 64;
-  const T* src = x + (int64_t)n * sn;
-  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
-    const int cc = i / 64, pp = i % 64;
-    const int c = c0 + cc, pix = p0 + pp;
-    tile[cc][pp] = (c < C && pix < HW) ? src[(int64_t)c * sc + pix] : T(0.f);
+  const int c0 = blockIdx.y * TC, p0 = blockIdx.x * TP;
+  const uint16_t* src = reinterpret_cast<const uint16_t*>(x) + (int64_t)n * sn;
+  const bool vec_ok = (sc % 8) == 0 && (HW % 8) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+  // load: thread handles 8 consecutive pixels of one channel
+  for (int i = threadIdx.x; i < TC * (TP / 8); i += blockDim.x) {
+    const int cc = i / (TP / 8), pv = (i % (TP / 8)) * 8;
+    const int c = c0 + cc, pix = p0 + pv;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (c < C) {
+      const uint16_t* g = src + (int64_t)c * sc + pix;
+      if (vec_ok && pix + 8 <= HW) {
+        v = *reinterpret_cast<const uint4*>(g);
+      } else {
+        uint16_t e[8];
+        for (int k = 0; k < 8; ++k) e[k] = pix + k < HW ? g[k] : (uint16_t)0;
+        v = make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16),
+                       e[6] | ((uint32_t)e[7] << 16));
+      }
+    }
+    *reinterpret_cast<uint4*>(&tile[cc][pv]) = v;
   }
   __syncthreads();
-  T* dst = out + (int64_t)n * HW * C8;
-  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
-    const int pp = i / 64, cc = i % 64;
-    const int c = c0 + cc, pix = p0 + pp;
-    if (c < C8 && pix < HW) dst[(int64_t)pix * C8 + c] = tile[cc][pp];
+  // store: thread handles 8 consecutive channels of one pixel
+  uint16_t* dst = reinterpret_cast<uint16_t*>(out) + (int64_t)n * HW * C8;
+  for (int i = threadIdx.x; i < TP * (TC / 8); i += blockDim.x) {
+    const int pp = i / (TC / 8), cv = (i % (TC / 8)) * 8;
+    const int c = c0 + cv, pix = p0 + pp;
+    if (pix >= HW || c >= C8) continue;
+    uint16_t e[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) e[k] = tile[cv + k][pp];
+    *reinterpret_cast<uint4*>(dst + (int64_t)pix * C8 + c) =
+        make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16),
+                   e[6] | ((uint32_t)e[7] << 16));
   }
 }
 
@@ -307,7 +331,7 @@ int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
   if (!nhwc) {
     // NCHW planes must be contiguous H*W runs for the transpose
     if (c.xs[3] != 1 || c.xs[2] != c.W) return NTB_ERR_UNSUPPORTED;
-    dim3 grid((unsigned)cdiv64(HW, 64), (unsigned)cdiv64(C8, 64), (unsigned)c.N);
+    dim3 grid((unsigned)cdiv64(HW, 128), (unsigned)cdiv64(C8, 64), (unsigned)c.N);
     if (bf16)
       nchw_to_nhwc<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)c.x, c.xs[0], c.xs[1],
                                                       (__nv_bfloat16*)xp, (int)c.C, (int)C8,

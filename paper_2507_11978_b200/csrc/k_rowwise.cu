@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) row_vec_kernel(const T* __restrict__ in, 
 // 8 x (S-1) rows (>= 100 KB) in flight - enough to cover HBM latency at full
 // bandwidth.  The warp reduces its row out of shared memory (warp shuffles,
 // fp32) and writes the result with 128-bit streaming stores.
-constexpr int kStreamWarps = 8;
+constexpr int kStreamWarps = 16;
 constexpr int kStreamMaxStages = 8;
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -283,7 +283,7 @@ static bool try_stream(const T* in, int64_t in_rs, const T* w, T* out, int64_t o
   const int64_t budget = 200 * 1024 - (kSoftmax ? 0 : row_pad);
   int64_t stages = budget / (kStreamWarps * row_pad);
   if (stages > kStreamMaxStages) stages = kStreamMaxStages;
-  if (stages < 2) return false;
+  if (stages < 1) return false;
   const size_t smem = (size_t)(kStreamWarps * stages * row_pad + (kSoftmax ? 0 : row_pad));
   auto kern = row_stream_kernel<T, kSoftmax>;
   static size_t attr = 0;
