@@ -35,8 +35,11 @@ namespace {
 constexpr int BM = 128, BN = 128;  // query rows per tile, keys per KV tile
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-// Polynomial exp2 offload: measured slower on B200 at D=128 (the softmax is
-// issue-bound, not SFU-bound: 8.54 ms vs 8.10 ms), so it is off.
+// Polynomial exp2 offload: measured slower on B200 at D=128 (8.54 ms vs
+// 8.10 ms: the softmax warps are issue-bound at ~4 instructions per score,
+// so adding ~9 FMA-pipe instructions for a quarter of the scores costs more
+// than the SFU time it saves), so it is off.  ex2.approx.f16x2 is no help
+// either: on sm_100a it is split into two MUFU.EX2.F16 plus repacking.
 constexpr bool kPolyExp = false;
 
 struct AttnMaps {
@@ -180,14 +183,16 @@ __global__ void __launch_bounds__(384, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
         const bool more = j + 1 < n_kv;
-        if (more) {
-          mbar_wait(&kv_full[st ^ 1], ((j + 1) >> 1) & 1);
-        }
         mbar_wait(&p_full[0], j & 1);
         tc_fence_after();
         issue_pv(0, j);
-        if (more) issue_s(0, j + 1);
-        else mma_commit(&o_full[0]);
+        if (more) {
+          mbar_wait(&kv_full[st ^ 1], ((j + 1) >> 1) & 1);   // K/V_{j+1} landed
+          tc_fence_after();
+          issue_s(0, j + 1);
+        } else {
+          mma_commit(&o_full[0]);
+        }
         mbar_wait(&p_full[1], j & 1);
         tc_fence_after();
         issue_pv(1, j);
