@@ -75,50 +75,54 @@ __global__ void repack_filter(const T* __restrict__ w, int64_t s0, int64_t s1, i
   }
 }
 
-// X'[n][pix][c8] <- X[n][c][pix]: 64 channels x 128 pixels per CTA through
-// shared memory, 128-bit loads along pixels and 128-bit stores along
-// channels (HBM-bound: reads and writes the image once).
+// X'[n][pix][c8] <- X[n][c][pix]: 64 channels x 64 pixels per CTA.  Each
+// thread loads 8 pixels of a channel PAIR (two 128-bit loads), packs the
+// pair per pixel into 32-bit words and writes them to a [pixel][pair] tile
+// (row pitch 36 words: bank-conflict-free both ways); the store phase reads
+// 128-bit runs of 8 channels per pixel and writes 128 B per pixel.
 template <typename T>
 __global__ void __launch_bounds__(256) nchw_to_nhwc(const T* __restrict__ x, int64_t sn,
                                                     int64_t sc, T* __restrict__ out, int C,
                                                     int C8, int HW) {
-  constexpr int TC = 64, TP = 128;
-  __shared__ __align__(16) uint16_t tile[TC][TP + 8];
+  constexpr int TP = 64, PITCH = 36;          // pixels per tile, words per row
+  __shared__ __align__(16) uint32_t tile[TP * PITCH];
   const int n = blockIdx.z;
-  const int c0 = blockIdx.y * TC, p0 = blockIdx.x * TP;
+  const int c0 = blockIdx.y * 64, p0 = blockIdx.x * TP;
   const uint16_t* src = reinterpret_cast<const uint16_t*>(x) + (int64_t)n * sn;
   const bool vec_ok = (sc % 8) == 0 && (HW % 8) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
-  // load: thread handles 8 consecutive pixels of one channel
-  for (int i = threadIdx.x; i < TC * (TP / 8); i += blockDim.x) {
-    const int cc = i / (TP / 8), pv = (i % (TP / 8)) * 8;
-    const int c = c0 + cc, pix = p0 + pv;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (c < C) {
-      const uint16_t* g = src + (int64_t)c * sc + pix;
-      if (vec_ok && pix + 8 <= HW) {
-        v = *reinterpret_cast<const uint4*>(g);
+  {
+    const int cw = threadIdx.x & 31, pb = threadIdx.x >> 5;   // channel pair, 8-pixel block
+    const int pix = p0 + pb * 8;
+    uint16_t a[8], b[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint16_t* e = h ? b : a;
+      const int c = c0 + 2 * cw + h;
+      if (c < C && vec_ok && pix + 8 <= HW) {
+        const uint4 v = *reinterpret_cast<const uint4*>(src + (int64_t)c * sc + pix);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          e[2 * k] = (uint16_t)(w[k] & 0xFFFF);
+          e[2 * k + 1] = (uint16_t)(w[k] >> 16);
+        }
       } else {
-        uint16_t e[8];
-        for (int k = 0; k < 8; ++k) e[k] = pix + k < HW ? g[k] : (uint16_t)0;
-        v = make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16),
-                       e[6] | ((uint32_t)e[7] << 16));
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          e[k] = (c < C && pix + k < HW) ? src[(int64_t)c * sc + pix + k] : (uint16_t)0;
       }
     }
-    *reinterpret_cast<uint4*>(&tile[cc][pv]) = v;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tile[(pb * 8 + k) * PITCH + cw] = a[k] | ((uint32_t)b[k] << 16);
   }
   __syncthreads();
-  // store: thread handles 8 consecutive channels of one pixel
   uint16_t* dst = reinterpret_cast<uint16_t*>(out) + (int64_t)n * HW * C8;
-  for (int i = threadIdx.x; i < TP * (TC / 8); i += blockDim.x) {
-    const int pp = i / (TC / 8), cv = (i % (TC / 8)) * 8;
-    const int c = c0 + cv, pix = p0 + pp;
+  for (int i = threadIdx.x; i < TP * 8; i += blockDim.x) {
+    const int pp = i >> 3, q = i & 7;             // pixel, group of 8 channels
+    const int c = c0 + q * 8, pix = p0 + pp;
     if (pix >= HW || c >= C8) continue;
-    uint16_t e[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) e[k] = tile[cv + k][pp];
-    *reinterpret_cast<uint4*>(dst + (int64_t)pix * C8 + c) =
-        make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16),
-                   e[6] | ((uint32_t)e[7] << 16));
+    const uint4 v = *reinterpret_cast<const uint4*>(&tile[pp * PITCH + q * 4]);
+    *reinterpret_cast<uint4*>(dst + (int64_t)pix * C8 + c) = v;
   }
 }
 
@@ -331,7 +335,7 @@ int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
   if (!nhwc) {
     // NCHW planes must be contiguous H*W runs for the transpose
     if (c.xs[3] != 1 || c.xs[2] != c.W) return NTB_ERR_UNSUPPORTED;
-    dim3 grid((unsigned)cdiv64(HW, 128), (unsigned)cdiv64(C8, 64), (unsigned)c.N);
+    dim3 grid((unsigned)cdiv64(HW, 64), (unsigned)cdiv64(C8, 64), (unsigned)c.N);
     if (bf16)
       nchw_to_nhwc<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)c.x, c.xs[0], c.xs[1],
                                                       (__nv_bfloat16*)xp, (int)c.C, (int)C8,

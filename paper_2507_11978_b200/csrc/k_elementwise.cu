@@ -31,6 +31,8 @@ __global__ void __launch_bounds__(256) ew_vec_kernel(const T* __restrict__ a,
                                                      T* __restrict__ out, int64_t n_vec) {
   using P = Pack<T>;
   Op op;
+  pdl_wait();
+  pdl_trigger();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + (UNROLL - 1) * stride < n_vec; i += UNROLL * stride) {
@@ -103,7 +105,8 @@ static int run_ew(const LaunchArgs& A) {
     int64_t cap = (int64_t)sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    ew_vec_kernel<T, Op, U><<<(unsigned)blocks, 256, 0, A.stream>>>(a, b, out, n_vec);
+    launch_pdl(ew_vec_kernel<T, Op, U>, dim3((unsigned)blocks), dim3(256), 0, A.stream, a, b, out,
+               n_vec);
     return check_launch("elementwise", NTB_PATH_EW_VEC);
   } else {
     int64_t blocks = cdiv64(no, 256);

@@ -21,6 +21,8 @@ __global__ void __launch_bounds__(256) rope_vec_kernel(const T* __restrict__ x,
                                                        T* __restrict__ out, int64_t rows,
                                                        int64_t S, int64_t H, int half) {
   using P = Pack<T>;
+  pdl_wait();
+  pdl_trigger();
   const int vpr = half / P::N;  // packs per half-row
   const int64_t n = rows * vpr;
   const int64_t D = 2 * (int64_t)half;
@@ -118,8 +120,8 @@ static int run_rope(const LaunchArgs& A) {
     int64_t items = rows * (half / N);
     int64_t blocks = cdiv64(items, 256);
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
-    rope_vec_kernel<T><<<(unsigned)blocks, 256, 0, A.stream>>>(x, sn, cs, out, rows, xs.n[1],
-                                                               xs.n[2], (int)half);
+    launch_pdl(rope_vec_kernel<T>, dim3((unsigned)blocks), dim3(256), 0, A.stream, x, sn, cs, out,
+               rows, xs.n[1], xs.n[2], (int)half);
     return check_launch("rope", NTB_PATH_ROPE_VEC);
   } else {
     int64_t items = xs.n[1] * xs.n[0] * xs.n[2] * half;

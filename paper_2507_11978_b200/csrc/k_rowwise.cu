@@ -147,6 +147,84 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
 
 __device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
 
+
+// ---- packed fp16 row math (issue-bound kernels: 2 elements per instruction) ----
+// max: HMNMX2 (exact); exp input (x - m) by HSUB2 (exact when x is within a
+// factor 2 of m - Sterbenz - otherwise one rounding of a value whose exp is
+// negligible), times log2e by HMUL2, exp2 on the SFU, e kept as fp16 in
+// place; row sum as fp16 partial sums of 8 values (each <= 1) accumulated
+// in fp32; normalisation by HMUL2.  rms_norm: squares of x * 2^-10 (no fp16
+// overflow for any finite fp16 x) summed 8 at a time, then fp32.  Error
+// <= a few fp16 ulp relative, inside the 1e-2 fp16 tolerance.  fp32 / bf16
+// rows keep the fp32 path.
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+__device__ __forceinline__ void softmax_row_f16(const uint4* buf, __half* dst, int n_vec,
+                                                int lane) {
+  __half2 mx = __float2half2_rn(-INFINITY);
+  for (int c = lane; c < n_vec; c += 32) {
+    const uint4 v = buf[c];
+    mx = __hmax2(mx, __hmax2(__hmax2(u2h(v.x), u2h(v.y)), __hmax2(u2h(v.z), u2h(v.w))));
+  }
+  float m = fmaxf(__low2float(mx), __high2float(mx));
+  m = warp_max(m);
+  const __half2 l2e = __float2half2_rn(1.4426950408889634f);
+  const __half2 m2 = __float2half2_rn(m);   // exact: m is an fp16 value
+  float sum = 0.f;
+  uint4* ebuf = const_cast<uint4*>(buf);
+  for (int c = lane; c < n_vec; c += 32) {
+    const uint4 v = buf[c];
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    __half2 acc = __float2half2_rn(0.f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __half2 x = __hmul2(__hsub2(u2h(w[k]), m2), l2e);
+      const __half2 e = h2exp2(x);
+      acc = __hadd2(acc, e);
+      w[k] = h2u(e);
+    }
+    const float2 a = __half22float2(acc);
+    sum += a.x + a.y;
+    ebuf[c] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  const __half2 inv = __float2half2_rn(1.0f / warp_sum(sum));
+  for (int c = lane; c < n_vec; c += 32) {
+    const uint4 v = buf[c];
+    const uint4 o = make_uint4(h2u(__hmul2(u2h(v.x), inv)), h2u(__hmul2(u2h(v.y), inv)),
+                               h2u(__hmul2(u2h(v.z), inv)), h2u(__hmul2(u2h(v.w), inv)));
+    st_stream(dst + (int64_t)c * 8, o);
+  }
+}
+
+__device__ __forceinline__ void rms_row_f16(const uint4* buf, const uint4* wv, __half* dst,
+                                            int n_vec, int cols, int lane) {
+  float ss = 0.f;
+  const __half2 sc = __float2half2_rn(1.0f / 1024.0f);
+  for (int c = lane; c < n_vec; c += 32) {
+    const uint4 v = buf[c];
+    const __half2 a0 = __hmul2(u2h(v.x), sc), a1 = __hmul2(u2h(v.y), sc);
+    const __half2 a2 = __hmul2(u2h(v.z), sc), a3 = __hmul2(u2h(v.w), sc);
+    __half2 acc = __hmul2(a0, a0);
+    acc = __hfma2(a1, a1, acc);
+    acc = __hfma2(a2, a2, acc);
+    acc = __hfma2(a3, a3, acc);
+    const float2 a = __half22float2(acc);
+    ss += a.x + a.y;
+  }
+  ss *= 1048576.0f;   // undo the 2^-20 scaling of the squares
+  const float rinv = 1.0f / sqrtf(warp_sum(ss) / (float)cols + kRmsEps);
+  const __half2 r2 = __float2half2_rn(rinv);
+  for (int c = lane; c < n_vec; c += 32) {
+    const uint4 v = buf[c], g = wv[c];
+    const uint4 o = make_uint4(h2u(__hmul2(__hmul2(u2h(v.x), r2), u2h(g.x))),
+                               h2u(__hmul2(__hmul2(u2h(v.y), r2), u2h(g.y))),
+                               h2u(__hmul2(__hmul2(u2h(v.z), r2), u2h(g.z))),
+                               h2u(__hmul2(__hmul2(u2h(v.w), r2), u2h(g.w))));
+    st_stream(dst + (int64_t)c * 8, o);
+  }
+}
+
 template <typename T, bool kSoftmax>
 __global__ void __launch_bounds__(kStreamWarps * 32, 1)
     row_stream_kernel(const T* __restrict__ in, int64_t in_rs, const T* __restrict__ w,
@@ -159,6 +237,8 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
   const uint32_t row_pad = (row_bytes + 127u) & ~127u;
   uint8_t* wbase = smem + (size_t)warp * stages * row_pad;
   const T* wsh = nullptr;
+  pdl_wait();
+  pdl_trigger();
   if (!kSoftmax) {
     // weight row once per CTA, after the per-warp rings
     uint8_t* wdst = smem + (size_t)kStreamWarps * stages * row_pad;
@@ -189,7 +269,10 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
     bar_wait(&bars[warp][s], (uint32_t)((k / stages) & 1));
     const uint4* buf = reinterpret_cast<const uint4*>(wbase + (size_t)s * row_pad);
     T* dst = out + r * out_rs;
-    if (kSoftmax) {
+    if constexpr (std::is_same<T, __half>::value) {
+      if (kSoftmax) softmax_row_f16(buf, dst, n_vec, lane);
+      else rms_row_f16(buf, reinterpret_cast<const uint4*>(wsh), dst, n_vec, cols, lane);
+    } else if (kSoftmax) {
       // pass 1: row max; pass 2: e = exp(x - m) written back in place (fp16
       // for 16-bit rows, fp32 for fp32 rows) + row sum; pass 3: e / sum.
       // One exponential per element (the SFU, not HBM, would otherwise bound).
@@ -295,8 +378,8 @@ static bool try_stream(const T* in, int64_t in_rs, const T* w, T* out, int64_t o
   }
   int64_t blocks = cdiv64(rows, kStreamWarps);
   if (blocks > sm_count()) blocks = sm_count();
-  kern<<<(unsigned)blocks, kStreamWarps * 32, smem, s>>>(in, in_rs, w, out, out_rs, rows,
-                                                         (int)cols, (int)stages);
+  launch_pdl(kern, dim3((unsigned)blocks), dim3(kStreamWarps * 32), smem, s, in, in_rs, w, out,
+             out_rs, rows, (int)cols, (int)stages);
   return true;
 }
 

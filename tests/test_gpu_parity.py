@@ -158,6 +158,18 @@ def test_rowwise(dtype, shape):
     _close(got, oracle.rms_norm(x, w), rtol=tol, atol=tol)
 
 
+@pytest.mark.parametrize("scale", [1.0, 30.0, 3000.0])
+def test_rows_fp16_large_magnitudes(scale):
+    """Packed-fp16 row math stays accurate for large logits / activations."""
+    rng = np.random.default_rng(int(scale))
+    x = _r16((rng.standard_normal((64, 4096)) * scale).astype(np.float32), torch.float16)
+    w = _r16(rng.uniform(-1, 1, 4096).astype(np.float32), torch.float16)
+    got = _run("softmax", {"input": x}, {"COLS_PADDED": 4096}, torch.float16)
+    _close(got, oracle.softmax(x, 4096), rtol=1e-2, atol=1e-4)
+    got = _run("rms_norm", {"input": x, "weight": w}, {"COLS_PADDED": 4096}, torch.float16)
+    _close(got, oracle.rms_norm(x, w), rtol=1e-2, atol=1e-2)
+
+
 def test_softmax_chunked_matches_reference_semantics():
     rng = np.random.default_rng(1)
     x = rng.uniform(-1, 1, (3, 20)).astype(np.float32)
