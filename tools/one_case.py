@@ -40,3 +40,11 @@ elif kind == "mm":
     torch.cuda.synchronize()
     print("mm", m, n, k, "max err", (c.float() - a.float() @ b.float()).abs().max().item(),
           {k_: v for k_, v in B.path_counts().items() if v})
+elif kind == "bmm":
+    bt, m, n, k = (int(x) for x in sys.argv[2:6])
+    a, b = T((bt, m, k)), T((bt, k, n))
+    c = torch.zeros((bt, m, n), device=dev, dtype=torch.float16)
+    for _ in range(3):
+        B.bmm_launch(a, b, c, 128, 128, 64)
+    torch.cuda.synchronize()
+    print("bmm max err", (c[:2].float() - a[:2].float() @ b[:2].float()).abs().max().item())
