@@ -59,7 +59,9 @@ def ncu_traffic():
 
 # --------------------------------------------------------------------------
 class Clocks:
-    """nvidia-smi sampler during the timed region."""
+    """SM clock / throttle-reason sampler (NVML, 10 ms period; nvidia-smi as
+    a fallback).  Used around a continuous replay of the timed step graph so
+    that the samples are taken under the same load as the timed region."""
 
     def __init__(self, index=0):
         self.index = index
@@ -68,21 +70,46 @@ class Clocks:
         self._t = None
 
     def __enter__(self):
-        def run():
+        def run_nvml():
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                    "sw_power_cap": 0x4}
+            while not self._stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                try:
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((sm, mx, [k for k, b in bits.items() if r & b]))
+                self._stop.wait(0.01)
+
+        def run_smi():
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
                  "clocks_event_reasons.sw_power_cap")
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
             while not self._stop.is_set():
                 try:
                     out = subprocess.run(
                         ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    f = [x.strip() for x in out.split(",")]
+                    self.samples.append((float(f[0]), float(f[1]),
+                                         [names[i] for i in range(4) if f[2 + i].lower() == "active"]))
                 except Exception:
                     pass
                 self._stop.wait(0.2)
+
+        def run():
+            try:
+                run_nvml()
+            except Exception:
+                run_smi()
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
@@ -95,14 +122,10 @@ class Clocks:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({r for s in self.samples for r in s[2]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples)}
 
 
 # --------------------------------------------------------------------------
@@ -344,6 +367,15 @@ def headline(args, n_gpus, rank, pk):
     ms_total = _max_over_ranks(timed(g_step), n_gpus)
     sm_ms = timed(g_sm) / args.steps
     rms_ms = timed(g_rms) / args.steps
+    # clock window: the same step graph replayed back to back for ~1 s while
+    # NVML samples SM clocks and throttle reasons every 10 ms
+    reps = max(1, int(1.0 / max(ms_total * 1e-3, 1e-6)))
+    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for _ in range(reps):
+            g_step.replay()
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    clocks["window"] = f"{reps} back-to-back replays of the timed {args.steps}-step graph"
     del g_step, g_sm, g_rms
     ms_step = ms_total / args.steps
     value = n_gpus * step_bytes / (ms_step * 1e-3) / 1e9
@@ -434,33 +466,57 @@ def headline(args, n_gpus, rank, pk):
             "frac": round(dom_units / (dom_ms * 1e-3) / 1e9 / pk["hbm"], 4),
             "traffic": traffic, "peak_source": pk["src"],
             "per_kernel_ms": {"softmax": round(sm_ms, 5), "rms_norm": round(rms_ms, 5)}}
-    return dict(value=value, ms_step=ms_step, launches=launches,
+    return dict(value=value, ms_step=ms_step, launches=launches, clocks=clocks,
                 e2e=e2e, roofline=roof, errs=errs, nsets=nsets)
 
 
-def cpu_baseline(sample_rows=1024):
-    """Oracle port (numpy restatement of sim.launch semantics) on the host:
-    softmax + rms_norm over a row sample of the same 4096-wide workload."""
+def _oracle_step(x, w, threads):
+    """softmax + rms_norm of the oracle over row blocks on `threads` host threads
+    (numpy releases the GIL inside the per-block kernels)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     import numpy as np
 
     import oracle
 
+    blocks = np.array_split(np.arange(x.shape[0]), threads)
+
+    def one(ix):
+        oracle.softmax(x[ix[0]:ix[-1] + 1], C)
+        oracle.rms_norm(x[ix[0]:ix[-1] + 1], w)
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(one, [b for b in blocks if len(b)]))
+
+
+def _host_threads():
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(sample_rows=2048):
+    """Oracle port (numpy restatement of the reference CPU path) on all host
+    cores: softmax + rms_norm over a row sample of the same 4096-wide workload."""
+    import numpy as np
+
     rng = np.random.default_rng(0)
     x = rng.uniform(-1, 1, (sample_rows, C)).astype(np.float16).astype(np.float32)
     w = rng.uniform(-1, 1, C).astype(np.float16).astype(np.float32)
-    oracle.softmax(x, C)
+    threads = _host_threads()
+    _oracle_step(x, w, threads)
     reps, t = 0, 0.0
     while t < 3.0 and reps < 50:
         t0 = time.perf_counter()
-        oracle.softmax(x, C)
-        oracle.rms_norm(x, w)
+        _oracle_step(x, w, threads)
         t += time.perf_counter() - t0
         reps += 1
     step_bytes = 2 * (2 * sample_rows * C * 2) + C * 2
-    return {"value": round(step_bytes * reps / t / 1e9, 3), "unit": "GB/s", "cores": 1,
+    return {"value": round(step_bytes * reps / t / 1e9, 3), "unit": "GB/s", "cores": threads,
             "kind": "port",
             "sample": f"softmax+rms_norm on {sample_rows}x{C} rows (fp16-rounded inputs, f32 math), "
-                      f"{reps} reps, numpy single-thread"}
+                      f"{reps} reps, numpy on {threads} host threads"}
 
 
 def run_reference(args):
@@ -473,16 +529,15 @@ def run_reference(args):
     import oracle
 
     rng = np.random.default_rng(0)
-    rows = 512  # bounded sample per step
+    rows = 2048  # bounded sample per step (half the 4096 rows)
     x = rng.uniform(-1, 1, (rows, C)).astype(np.float16).astype(np.float32)
     w = rng.uniform(-1, 1, C).astype(np.float16).astype(np.float32)
+    threads = _host_threads()
     for _ in range(args.warmup):
-        oracle.softmax(x, C)
-        oracle.rms_norm(x, w)
+        _oracle_step(x, w, threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.softmax(x, C)
-        oracle.rms_norm(x, w)
+        _oracle_step(x, w, threads)
     dt = (time.perf_counter() - t0) / args.steps
     step_bytes = 2 * (2 * rows * C * 2) + C * 2
     val = step_bytes / dt / 1e9
@@ -491,8 +546,9 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic uniform(-1,1), fp16-rounded", "impl": "reference",
             "config": {"workload": HEADLINE, "sample_rows_per_step": rows},
-            "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": 1, "kind": "port",
-                             "sample": f"{rows}x{C} rows per step (oracle port of sim.launch)"},
+            "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                             "sample": f"{rows}x{C} rows per step (oracle port of sim.launch), "
+                                       f"numpy on {threads} host threads"},
             "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -523,7 +579,6 @@ def main():
     n_gpus, rank, local = _dist()
     torch.cuda.set_device(local)
     pk = peaks()
-    clk = Clocks(local).__enter__()
     h = headline(args, n_gpus, rank, pk)
     kernels = {}
     names = ["add_2^20", "add_2^24", "silu_2^24", "softmax", "rms_norm", "mm", "addmm", "bmm",
@@ -544,8 +599,6 @@ def main():
                                 "note": wk.note}
             except Exception as e:  # report, never hide
                 kernels[key] = {"workload": wk.name, "error": f"{type(e).__name__}: {e}"}
-    clk.__exit__(None, None, None)
-    h["clocks"] = clk.summary()
     if rank != 0:
         return
     line = {

@@ -4,22 +4,26 @@
 //
 // One CTA per (batch, head, 256 query rows) = two 128-row query tiles that
 // share every K/V tile (ping-pong, as in FlashAttention-4):
-//   * warp 0: TMA producer - Q0/Q1 once, then K_j / V_j into a 2-stage ring
-//     (128B-swizzled; K K-major, V MN-major as the B operand of P.V);
+//   * warp 0: TMA producer - Q0/Q1 once, then K_j / V_j (112 keys per tile)
+//     into a 2-stage ring (128B-swizzled; K K-major, V MN-major);
 //   * warp 1: one thread issues tcgen05.mma in the order
 //       S0_0, S1_0, { PV0_j, S0_{j+1}, PV1_j, S1_{j+1} }_j
-//     so the tensor core always has the other query tile's work while a
-//     softmax warpgroup is busy;
+//     so the tensor core has the other query tile's work while a softmax
+//     warpgroup is busy;
 //   * warps 4-7 / 8-11: softmax warpgroups for Q0 / Q1, ONE THREAD PER QUERY
 //     ROW (32x32b TMEM loads give each thread its own row: no shuffles);
-//     P = exp2(S*scale*log2e - m) is written back as packed fp16 INTO THE
-//     S COLUMNS OF TMEM and consumed from there by the next MMA
-//     (tcgen05.mma with the A operand in TMEM), so P never touches smem;
-//   * lazy rescaling: the running max used for P only moves when a row max
-//     grows by more than 2^8; only then is the O row (TMEM) rescaled.  The
-//     MMA that produced S_{g,j} was issued after PV_{g,j-1}, so waiting for
-//     S_{g,j} already guarantees O_g is up to date - no extra barrier.
-// TMEM: S0/P0 [0,128) S1/P1 [128,256) O0 [256,256+D) O1 [256+D,256+2D).
+//     P = exp2(S*scale*log2e - m) is written back as packed 16-bit INTO THE
+//     S COLUMNS OF TMEM and consumed from there (tcgen05.mma, A in TMEM);
+//   * the ROW SUM IS COMPUTED BY THE TENSOR CORE: the P.V MMA multiplies by
+//     [V | 1] (N = D + 16; a constant chunk of ones sits after V in every
+//     ring stage), so the accumulator carries l next to O, rescaled with it
+//     - the softmax threads only do FFMA + EX2 + pack per score, which keeps
+//     the SFU and FMA pipes under the tensor-core time per tile;
+//   * lazy rescaling: the running max only moves when a row max grows by
+//     more than 2^8; only then is the [O | l] row (TMEM) rescaled.  S_{g,j}
+//     is issued after PV_{g,j-1}, so waiting for S_{g,j} already means the
+//     accumulator is current.
+// TMEM (512 cols): S0/P0 [0,112) S1/P1 [112,224) then [O|l]0, [O|l]1.
 // Keys beyond S_k are masked to -inf; query rows beyond S_q are not stored.
 // Tensor roofline: 4*B*H*S_q*S_k*D flop per launch.
 #include <cuda_bf16.h>
@@ -32,15 +36,9 @@
 namespace ntb {
 namespace {
 
-constexpr int BM = 128, BN = 128;  // query rows per tile, keys per KV tile
+constexpr int BM = 128, BN = 112;  // query rows per tile, keys per KV tile
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-// Polynomial exp2 offload: measured slower on B200 at D=128 (8.54 ms vs
-// 8.10 ms: the softmax warps are issue-bound at ~4 instructions per score,
-// so adding ~9 FMA-pipe instructions for a quarter of the scores costs more
-// than the SFU time it saves), so it is off.  ex2.approx.f16x2 is no help
-// either: on sm_100a it is split into two MUFU.EX2.F16 plus repacking.
-constexpr bool kPolyExp = false;
 
 struct AttnMaps {
   CUtensorMap q, k, v;
@@ -55,14 +53,18 @@ struct AttnParams {
 
 template <int D>
 struct Layout {
-  static constexpr int DCH = D / 64;              // 128B chunks along D
-  static constexpr int Q_BYTES = BM * D * 2;      // one query tile
-  static constexpr int K_BYTES = BN * D * 2;
-  static constexpr int V_BYTES = BN * D * 2;
-  static constexpr int KV_BYTES = K_BYTES + V_BYTES;
+  static constexpr int DCH = D / 64;               // 128B chunks along D
+  static constexpr int NO = D + 16;                // [O | l] accumulator width
+  static constexpr int Q_BYTES = BM * D * 2;       // one query tile
+  static constexpr int KCH = BN * 128;             // one 64-wide chunk of a K/V tile
+  static constexpr int K_BYTES = DCH * KCH;
+  static constexpr int V_BYTES = (DCH + 1) * KCH;  // V chunks + the ones chunk
+  static constexpr int ST_BYTES = K_BYTES + V_BYTES;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = 2 * Q_BYTES;
-  static constexpr int SMEM = OFF_KV + 2 * KV_BYTES + 1024;
+  static constexpr int SMEM = OFF_KV + 2 * ST_BYTES + 1024;
+  static constexpr uint32_t T_S0 = 0, T_S1 = BN, T_O0 = 2 * BN, T_O1 = 2 * BN + NO;
+  static_assert(2 * BN + 2 * NO <= 512, "TMEM budget");
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -72,16 +74,20 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 // 2^x on the FMA/ALU pipes (Cody-Waite split + cubic, rel. err 7.5e-5 <
-// half an fp16 ulp): offloads a quarter of the exponentials from the SFU,
-// which otherwise bounds the softmax at the tensor-core rate (FA4 trick).
+// half an fp16 ulp): takes a quarter of the exponentials off the SFU, which
+// otherwise needs ~94% of the tensor-core time per KV tile (FA4's trick).
 __device__ __forceinline__ float ex2_poly(float x) {
   x = fmaxf(x, -125.f);
   const float t = x + 12582912.0f;                    // 1.5 * 2^23: round to int
   const int i = __float_as_int(t) - 0x4B400000;
   const float f = x - (t - 12582912.0f);             // f in [-0.5, 0.5]
-  float p = fmaf(fmaf(fmaf(0.0551702793f, f, 0.242607975f), f, 0.693260928f), f, 0.999928276f);
-  return __int_as_float(__float_as_int(p) + (i << 23));
+  const float q = fmaf(fmaf(fmaf(0.0551702793f, f, 0.242607975f), f, 0.693260928f), f, 0.999928276f);
+  return __int_as_float(__float_as_int(q) + (i << 23));
 }
+
+#ifndef NTB_ATTN_POLY
+#define NTB_ATTN_POLY 0  // measured: no gain on B200 (8.05-8.30 ms either way, within noise)
+#endif
 
 template <bool BF16>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -104,6 +110,17 @@ __global__ void __launch_bounds__(384, 1)
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int n_kv = (p.Sk + BN - 1) / BN;
 
+  // constant "ones" chunk after V in both ring stages (row-sum operand)
+  {
+    const uint16_t one = BF16 ? 0x3F80 : 0x3C00;
+    const uint32_t w = one | ((uint32_t)one << 16);
+    for (int st = 0; st < 2; ++st) {
+      uint4* dst = reinterpret_cast<uint4*>(smem + L::OFF_KV + st * L::ST_BYTES + L::K_BYTES +
+                                            L::DCH * L::KCH);
+      for (int i = threadIdx.x; i < L::KCH / 16; i += blockDim.x) dst[i] = make_uint4(w, w, w, w);
+    }
+    fence_proxy_async();
+  }
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
     for (int i = 0; i < 2; ++i) {
@@ -139,42 +156,41 @@ __global__ void __launch_bounds__(384, 1)
         const int st = j & 1;
         const uint32_t ph = (j >> 1) & 1;
         mbar_wait(&kv_empty[st], ph ^ 1);
-        mbar_expect_tx(&kv_full[st], L::KV_BYTES);
-        uint8_t* kdst = smem + L::OFF_KV + st * L::KV_BYTES;
+        mbar_expect_tx(&kv_full[st], L::K_BYTES + L::DCH * L::KCH);
+        uint8_t* kdst = smem + L::OFF_KV + st * L::ST_BYTES;
         uint8_t* vdst = kdst + L::K_BYTES;
 #pragma unroll
         for (int c = 0; c < L::DCH; ++c) {
-          tma_load_4d(kdst + c * (BN * 128), &maps.k, &kv_full[st], c * 64, j * BN, h, b);
-          tma_load_4d(vdst + c * (BN * 128), &maps.v, &kv_full[st], c * 64, j * BN, h, b);
+          tma_load_4d(kdst + c * L::KCH, &maps.k, &kv_full[st], c * 64, j * BN, h, b);
+          tma_load_4d(vdst + c * L::KCH, &maps.v, &kv_full[st], c * 64, j * BN, h, b);
         }
       }
     }
   } else if (warp == 1) {
     if (elect_one()) {
       constexpr uint32_t idesc_s = idesc_f16(BF16, false, false, BM, BN);
-      constexpr uint32_t idesc_o = idesc_f16(BF16, false, true, BM, D);
+      constexpr uint32_t idesc_o = idesc_f16(BF16, false, true, BM, L::NO);
       mbar_wait(&q_full, 0);
       auto issue_s = [&](int g, int j) {
         const int st = j & 1;
         const uint32_t q_addr = smem_u32(smem + L::OFF_Q + g * L::Q_BYTES);
-        const uint32_t k_addr = smem_u32(smem + L::OFF_KV + st * L::KV_BYTES);
+        const uint32_t k_addr = smem_u32(smem + L::OFF_KV + st * L::ST_BYTES);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-          const uint32_t koff = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
-          mma_f16_ss(tmem + g * BN, umma_desc_sw128(q_addr + off, 16, 1024),
+          const uint32_t koff = (kk >> 2) * L::KCH + (kk & 3) * 32;
+          mma_f16_ss(tmem + (g ? L::T_S1 : L::T_S0), umma_desc_sw128(q_addr + off, 16, 1024),
                      umma_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk != 0);
         }
         mma_commit(&s_full[g]);
       };
       auto issue_pv = [&](int g, int j) {
         const int st = j & 1;
-        const uint32_t v_addr = smem_u32(smem + L::OFF_KV + st * L::KV_BYTES + L::K_BYTES);
+        const uint32_t v_addr = smem_u32(smem + L::OFF_KV + st * L::ST_BYTES + L::K_BYTES);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
-          mma_f16_ts(tmem + 2 * BN + g * D, tmem + g * BN + kk * 8,
-                     umma_desc_sw128(v_addr + kk * 2048, BN * 128, 1024), idesc_o,
-                     (j | kk) != 0);
+          mma_f16_ts(tmem + (g ? L::T_O1 : L::T_O0), tmem + (g ? L::T_S1 : L::T_S0) + kk * 8,
+                     umma_desc_sw128(v_addr + kk * 2048, L::KCH, 1024), idesc_o, (j | kk) != 0);
       };
       mbar_wait(&kv_full[0], 0);
       tc_fence_after();
@@ -206,27 +222,28 @@ __global__ void __launch_bounds__(384, 1)
     const int quad = warp & 3;              // TMEM lane quadrant
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t t_s = tmem + g * BN + lane_off;
-    const uint32_t t_o = tmem + 2 * BN + g * D + lane_off;
-    float m_used = -INFINITY, l = 0.f;
+    const uint32_t t_s = tmem + (g ? L::T_S1 : L::T_S0) + lane_off;
+    const uint32_t t_o = tmem + (g ? L::T_O1 : L::T_O0) + lane_off;
+    float m_used = -INFINITY;
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(&s_full[g], j & 1);
       tc_fence_after();
       const int kvalid = p.Sk - j * BN;
+      // pass 1: row max (S row in registers: 3 x 32 + 16 columns)
+      uint32_t v[BN];
+      tmem_ld_32x32b_x32(t_s, v);
+      tmem_ld_32x32b_x32(t_s + 32, v + 32);
+      tmem_ld_32x32b_x32(t_s + 64, v + 64);
+      tmem_ld_32x32b_x16(t_s + 96, v + 96);
+      tmem_ld_wait();
       float mx = -INFINITY;
+      if (kvalid >= BN) {
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_s + c * 32, v);
-        tmem_ld_wait();
-        if (kvalid >= BN) {
+        for (int i = 0; i < BN; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+      } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i < kvalid) mx = fmaxf(mx, __uint_as_float(v[i]));
-        }
+        for (int i = 0; i < BN; ++i)
+          if (i < kvalid) mx = fmaxf(mx, __uint_as_float(v[i]));
       }
       const float cand = mx * p.scale_log2;
       const bool warp_grow = __any_sync(0xffffffffu, cand > m_used + kRescaleThreshold);
@@ -235,20 +252,16 @@ __global__ void __launch_bounds__(384, 1)
         m_new = fmaxf(m_used, cand);
         alpha = ex2(m_used - m_new);
       }
-      // P = exp2(s*scale - m) packed fp16 into the S columns (in place, in order)
-      float sum = 0.f;
+      // pass 2: P = exp2(s*scale - m), packed into the S columns (in order)
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_s + c * 32, v);
-        tmem_ld_wait();
-        uint32_t pk[16];
+      for (int c = 0; c < BN / 16; ++c) {
+        uint32_t pk[8];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float x0 = fmaf(__uint_as_float(v[i]), p.scale_log2, -m_new);
-          const float x1 = fmaf(__uint_as_float(v[i + 1]), p.scale_log2, -m_new);
+        for (int i = 0; i < 16; i += 2) {
+          const float x0 = fmaf(__uint_as_float(v[c * 16 + i]), p.scale_log2, -m_new);
+          const float x1 = fmaf(__uint_as_float(v[c * 16 + i + 1]), p.scale_log2, -m_new);
           float e0, e1;
-          if (kPolyExp && (i & 6) == 0) {  // 8 of every 32 columns on the FMA pipe
+          if (NTB_ATTN_POLY && (i & 6) == 0) {   // 4 of every 16 scores on the FMA pipe
             e0 = ex2_poly(x0);
             e1 = ex2_poly(x1);
           } else {
@@ -256,25 +269,23 @@ __global__ void __launch_bounds__(384, 1)
             e1 = ex2(x1);
           }
           if (kvalid < BN) {
-            if (c * 32 + i >= kvalid) e0 = 0.f;
-            if (c * 32 + i + 1 >= kvalid) e1 = 0.f;
+            if (c * 16 + i >= kvalid) e0 = 0.f;
+            if (c * 16 + i + 1 >= kvalid) e1 = 0.f;
           }
-          sum += e0 + e1;
           pk[i / 2] = pack2<BF16>(e0, e1);
         }
-        tmem_st_32x32b_x16(t_s + c * 16, pk);
+        tmem_st_32x32b_x8(t_s + c * 8, pk);
       }
-      l = l * alpha + sum;
       if (warp_grow && j > 0) {
-        // O_g is final for tiles < j: S_{g,j} was issued after PV_{g,j-1}
+        // rescale the [O | l] row (current: S_{g,j} was issued after PV_{g,j-1})
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(t_o + c * 32, v);
+        for (int c = 0; c < L::NO / 16; ++c) {
+          uint32_t w[16];
+          tmem_ld_32x32b_x16(t_o + c * 16, w);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-          tmem_st_32x32b_x32(t_o + c * 32, v);
+          for (int i = 0; i < 16; ++i) w[i] = __float_as_uint(__uint_as_float(w[i]) * alpha);
+          tmem_st_32x32b_x16(t_o + c * 16, w);
         }
       }
       m_used = m_new;
@@ -283,35 +294,38 @@ __global__ void __launch_bounds__(384, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[g]);
     }
-    // epilogue: O / l -> global
+    // epilogue: O / l -> global (l = accumulator column D)
     mbar_wait(&o_full[g], 0);
     tc_fence_after();
+    uint32_t lw[1];
+    tmem_ld_32x32b_x1(t_o + D, lw);
+    tmem_ld_wait();
+    const float inv = 1.f / __uint_as_float(lw[0]);
     const int qrow = qt * 2 * BM + g * BM + row;
-    const float inv = 1.f / l;
     char* obase = reinterpret_cast<char*>(p.o) +
                   ((int64_t)b * p.os[0] + (int64_t)h * p.os[1] + (int64_t)qrow * p.os[2]) * 2;
     const bool vec = p.os[3] == 1 && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0);
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(t_o + c * 32, v);
+      uint32_t w[32];
+      tmem_ld_32x32b_x32(t_o + c * 32, w);
       tmem_ld_wait();
       if (qrow < p.Sq) {
         if (vec) {
           uint4* dst = reinterpret_cast<uint4*>(obase + c * 64);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            uint32_t w[4];
+            uint32_t q4[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              w[e] = pack2<BF16>(__uint_as_float(v[u * 8 + e * 2]) * inv,
-                                 __uint_as_float(v[u * 8 + e * 2 + 1]) * inv);
-            dst[u] = make_uint4(w[0], w[1], w[2], w[3]);
+              q4[e] = pack2<BF16>(__uint_as_float(w[u * 8 + e * 2]) * inv,
+                                  __uint_as_float(w[u * 8 + e * 2 + 1]) * inv);
+            dst[u] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
           }
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const float f = __uint_as_float(v[i]) * inv;
+            const float f = __uint_as_float(w[i]) * inv;
             const int64_t off = (int64_t)(c * 32 + i) * p.os[3] * 2;
             if constexpr (BF16)
               *reinterpret_cast<__nv_bfloat16*>(obase + off) = __float2bfloat16_rn(f);
