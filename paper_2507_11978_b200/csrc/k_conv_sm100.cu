@@ -41,7 +41,7 @@ constexpr int A_BYTES = 128 * BK * 2;
 constexpr int B_BYTES = 128 * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int XPOSE_FLOATS = 32 * 33;                       // per epilogue warp
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4 * XPOSE_FLOATS * 4 + 1024;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // + static xpose buffer
 constexpr int TMEM_COLS = 512;
 
 struct ConvMaps {
@@ -135,7 +135,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  float* xpose = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  // static (not carved from the dynamic buffer) so the compiler keeps the
+  // shared address space: LDS/STS instead of generic LD/ST + MEMBARs
+  __shared__ float xpose[4 * XPOSE_FLOATS];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
 

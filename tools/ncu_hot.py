@@ -6,12 +6,14 @@ import sys
 
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
+if len(sys.argv) > 3:
+    cmd += ["--kernel-name", f"regex:{sys.argv[3]}"]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 ia, isrc, iss = hdr.index("Address"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
-body = [r for r in rows[2:] if len(r) == len(hdr)]
+body = [r for r in rows[2:] if len(r) == len(hdr) and r[iss].isdigit()]
 tot = sum(int(r[iss] or 0) for r in body)
 print("total samples", tot)
 for i, r in sorted(enumerate(body), key=lambda x: -int(x[1][iss] or 0))[:n]:
