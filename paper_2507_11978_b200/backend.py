@@ -81,30 +81,142 @@ _cache_lock = threading.Lock()
 _cache: dict = {}
 
 
+def _rename_tree(t, ren):
+    """JSON-form expression tree with symbols renamed."""
+    if t[0] == "sym":
+        return ["sym", ren.get(t[1], t[1])]
+    if t[0] == "const":
+        return list(t)
+    return [t[0]] + [_rename_tree(a, ren) for a in t[1:]]
+
+
+def _canon_ir(node, ren, params, scope):
+    """ir_tree() output with parameters positional and locals / loop
+    variables numbered by first appearance (alpha-renaming)."""
+    if isinstance(node, list) and node and isinstance(node[0], str) and node[0] == "expr":
+        return ["expr", _rename_tree(node[1], ren)]
+    if isinstance(node, list) and node and isinstance(node[0], str) and node[0][:1].isupper():
+        cls = node[0]
+        out = [cls]
+        for field, value in node[1:]:
+            if field == "param":
+                value = params.get(value, value)
+            elif field == "name" and cls in ("Let", "Assign", "Accumulate", "Local", "Var"):
+                value = scope.setdefault(("l", value), f"l{len(scope)}")
+            elif field == "var" and cls == "ForRange":
+                value = scope.setdefault(("l", value), f"l{len(scope)}")
+            else:
+                value = _canon_ir(value, ren, params, scope)
+            out.append([field, value])
+        return out
+    if isinstance(node, list):
+        return [_canon_ir(x, ren, params, scope) for x in node]
+    return node
+
+
+def _inline_lets(stmts):
+    """Inline every single-assignment local (Let never Accumulate'd or
+    Assign'ed) into its uses, on the ir_tree() form, so that equivalent
+    formulations of the same application (e.g. the paper's softmax with its
+    `row_minus_max` temporaries vs the catalog's) compare equal."""
+    mutable = set()
+
+    def scan(n):
+        if isinstance(n, list) and n and isinstance(n[0], str) and n[0] in ("Accumulate", "Assign"):
+            mutable.add(dict(n[1:])["name"])
+        if isinstance(n, list):
+            for x in n:
+                scan(x)
+
+    scan(stmts)
+    defs = {}
+
+    def sub(n):
+        if isinstance(n, list) and n and n[0] == "Local":
+            name = dict(n[1:])["name"]
+            if name in defs:
+                return defs[name]
+        if isinstance(n, list):
+            return [sub(x) for x in n]
+        return n
+
+    def block(ss):
+        out = []
+        for st in ss:
+            if isinstance(st, list) and st and st[0] == "Let":
+                f = dict(st[1:])
+                if f["name"] not in mutable:
+                    defs[f["name"]] = sub(f["expr"])
+                    continue
+            if isinstance(st, list) and st and st[0] == "ForRange":
+                st = [st[0]] + [[k, block(v) if k == "body" else sub(v)] for k, v in st[1:]]
+                out.append(st)
+                continue
+            out.append(sub(st))
+        return out
+
+    return block(stmts)
+
+
 def _fingerprint(checked):
-    """Structural identity of a CheckedSpec: grid, checks, maps, IR."""
+    """Structural identity of a CheckedSpec - grid, checks, maps, IR - with
+    parameter, meta, local and kernel names factored out, so that any spec
+    that computes the same thing (e.g. one written through make()) matches."""
     spec = checked.spec
+    ren, params = {}, {}
+    for i, p in enumerate(spec.params):
+        params[p.name] = f"p{i}"
+        for d in range(p.rank):
+            ren[f"{p.name}_size_{d}"] = f"p{i}_size_{d}"
+            ren[f"{p.name}_stride_{d}"] = f"p{i}_stride_{d}"
+    for j, m in enumerate(spec.meta):
+        ren[m] = f"m{j}"
+
+    def tr(e):
+        return repr(_rename_tree(se.to_tree(se.from_any(e)), ren))
+
     maps = []
     for p in spec.params:
         if p.rank < 1:
             continue
         m = checked.index_maps[p.name]
         maps.append((
-            p.name,
-            tuple(se.from_any(s).node for s in m.lane_sizes),
-            tuple(se.from_any(s).node for s in m.nest_sizes),
-            se.from_any(m.offset).node,
-            tuple((se.from_any(a).node, se.from_any(b).node) for a, b in m.mask),
+            params[p.name],
+            tuple(tr(s) for s in m.lane_sizes),
+            tuple(tr(s) for s in m.nest_sizes),
+            tr(m.offset),
+            tuple((tr(a), tr(b)) for a, b in m.mask),
         ))
     return (
-        spec.name,
-        tuple((p.name, p.rank, p.role) for p in spec.params),
-        tuple(spec.meta),
-        tuple(se.from_any(s).node for s in checked.grid.sizes),
-        tuple((se.from_any(a).node, se.from_any(b).node) for a, b in checked.grid.checks),
+        tuple((p.rank, p.role) for p in spec.params),
+        len(spec.meta),
+        tuple(tr(s) for s in checked.grid.sizes),
+        tuple((tr(a), tr(b)) for a, b in checked.grid.checks),
         tuple(maps),
-        repr(ir_tree(spec.application)),
+        repr(_canon_ir(_inline_lets(ir_tree(spec.application)), ren, params, {})),
     )
+
+
+_canon_fps: dict = {}
+
+
+def _family_of(checked) -> str:
+    fp = _fingerprint(checked)
+    name = checked.spec.name
+    if name in ALL_NAMES:
+        if name not in _canon_fps:
+            _canon_fps[name] = _fingerprint(canonical(name))
+        if _canon_fps[name] == fp:
+            return name
+    for fam in ALL_NAMES:
+        if fam not in _canon_fps:
+            _canon_fps[fam] = _fingerprint(canonical(fam))
+        if _canon_fps[fam] == fp:
+            return fam
+    raise UnsupportedSpecError(
+        f"spec {name!r} does not match any sm_100a kernel family (add, silu, softmax, rms_norm, "
+        "mm, bmm, addmm, conv2d, sdpa, rope); the B200 backend executes only specs whose "
+        "arrangement and application it has a native kernel for")
 
 
 def _resolve(checked) -> tuple:
@@ -113,17 +225,11 @@ def _resolve(checked) -> tuple:
         hit = _cache.get(key)
         if hit is not None and hit[0] is checked:
             return hit[1], hit[2]
-    name = checked.spec.name
-    if name not in ALL_NAMES:
-        raise UnsupportedSpecError(f"no sm_100a kernel family for spec {name!r}")
-    if _fingerprint(checked) != _fingerprint(canonical(name)):
-        raise UnsupportedSpecError(
-            f"spec {name!r} does not match the canonical {name} arrangement/application; "
-            "the B200 backend only executes specs whose maps it has a native kernel for")
+    family = _family_of(checked)
     prog = build_program(checked)
     with _cache_lock:
-        _cache[key] = (checked, name, prog)
-    return name, prog
+        _cache[key] = (checked, family, prog)
+    return family, prog
 
 
 # ---- binding and validation (sim.py:120-160) ------------------------------
