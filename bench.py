@@ -367,6 +367,13 @@ def headline(args, n_gpus, rank, pk):
     ms_total = _max_over_ranks(timed(g_step), n_gpus)
     sm_ms = timed(g_sm) / args.steps
     rms_ms = timed(g_rms) / args.steps
+    # size-matched speed of light: a plain device copy of the same bytes
+    # (torch's copy kernel, same rotating sets) - what HBM gives a 67 MB
+    # read+write stream once launch, ramp and drain are paid
+    g_cp, _ = _graph(lambda i: sets[i % nsets]["ya"].copy_(sets[i % nsets]["xa"]), args.steps)
+    g_cp.replay()
+    copy_ms = min(timed(g_cp) for _ in range(3)) / args.steps
+    del g_cp
     # clock window: the same step graph replayed back to back for ~1 s while
     # NVML samples SM clocks and throttle reasons every 10 ms
     reps = max(1, int(1.0 / max(ms_total * 1e-3, 1e-6)))
@@ -465,7 +472,12 @@ def headline(args, n_gpus, rank, pk):
             "peak": pk["hbm"], "unit": "GB/s",
             "frac": round(dom_units / (dom_ms * 1e-3) / 1e9 / pk["hbm"], 4),
             "traffic": traffic, "peak_source": pk["src"],
-            "per_kernel_ms": {"softmax": round(sm_ms, 5), "rms_norm": round(rms_ms, 5)}}
+            "per_kernel_ms": {"softmax": round(sm_ms, 5), "rms_norm": round(rms_ms, 5)},
+            "size_matched_copy": {
+                "what": "torch copy_ of one 4096x4096 fp16 matrix (same bytes as one row kernel)",
+                "ms": round(copy_ms, 5),
+                "GB/s": round(2 * R * C * 2 / (copy_ms * 1e-3) / 1e9, 1),
+                "kernel_frac_of_copy": round(copy_ms / dom_ms, 4)}}
     return dict(value=value, ms_step=ms_step, launches=launches, clocks=clocks,
                 e2e=e2e, roofline=roof, errs=errs, nsets=nsets)
 

@@ -12,6 +12,9 @@ from pathlib import Path
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libntb200.so"
+# tuning sweeps only: load an alternative in-tree build (tools/build_variant.py)
+if os.environ.get("NTB_LIB_VARIANT"):
+    LIB_PATH = LIB_PATH.with_name(f"libntb200_{os.environ['NTB_LIB_VARIANT']}.so")
 
 NTB_OK, NTB_ERR_ARG, NTB_ERR_CHECK, NTB_ERR_UNSUPPORTED, NTB_ERR_CUDA, NTB_ERR_EVAL = range(6)
 NTB_F32, NTB_F16, NTB_BF16 = 0, 1, 2

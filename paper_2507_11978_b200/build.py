@@ -33,17 +33,21 @@ def _digest() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: tuple = ()) -> Path:
+    """Build libntb200.so; with ``variant`` build libntb200_<variant>.so with
+    extra -D ``defines`` instead (tuning sweeps, selected by NTB_LIB_VARIANT)."""
     OUT_DIR.mkdir(exist_ok=True)
-    stamp = OUT_DIR / "libntb200.sha256"
-    dig = _digest()
-    if LIB.exists() and stamp.exists() and stamp.read_text() == dig and not force:
-        return LIB
+    lib = LIB if variant is None else OUT_DIR / f"libntb200_{variant}.so"
+    stamp = OUT_DIR / (lib.stem + ".sha256")
+    dig = _digest() + repr(defines)
+    if lib.exists() and stamp.exists() and stamp.read_text() == dig and not force:
+        return lib
     objs = []
 
     def compile_one(src: Path):
-        obj = OUT_DIR / (src.stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = OUT_DIR / (src.stem + (f".{variant}" if variant else "") + ".o")
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -55,7 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static",
+    cmd = [NVCC, *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-lcudart_static",
            "-ldl", "-lrt", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -63,8 +67,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for o in objs:
         o.unlink(missing_ok=True)
     stamp.write_text(dig)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2507_11978_b200.build [--force] [-v] [--variant TAG -DNAME=VAL ...]
+    argv = sys.argv[1:]
+    var = argv[argv.index("--variant") + 1] if "--variant" in argv else None
+    defs = tuple(a[2:] for a in argv if a.startswith("-D"))
+    print(build(force="--force" in argv, verbose="-v" in argv, variant=var, defines=defs))

@@ -1,33 +1,38 @@
 // scaled_dot_product_attention on the sm_100a tensor cores (builder-defined
 // spec: the reference declares sdpa out of scope, catalog.py:36; the paper's
-// sdpa is FlashAttention-2).
+// sdpa is FlashAttention-2).  Version 4.
 //
-// One CTA per (batch, head, 256 query rows) = two 128-row query tiles that
-// share every K/V tile (ping-pong, as in FlashAttention-4):
-//   * warp 0: TMA producer - Q0/Q1 once, then K_j / V_j (112 keys per tile)
-//     into a 2-stage ring (128B-swizzled; K K-major, V MN-major);
+// Persistent CTAs (one per SM) walk work items (b, h, 256 query rows); each
+// item is two 128-row query tiles that share every K/V tile (ping-pong, as
+// in FlashAttention-4):
+//   * warp 0: TMA producer - Q0/Q1 per item, then K_j and V_j as SEPARATE
+//     ring entries (128 keys each, 128B-swizzled; K K-major, V MN-major) in
+//     a 5-slot ring (D = 128), so K_{j+1} can land while V_j is still in use;
 //   * warp 1: one thread issues tcgen05.mma in the order
 //       S0_0, S1_0, { PV0_j, S0_{j+1}, PV1_j, S1_{j+1} }_j
 //     so the tensor core has the other query tile's work while a softmax
-//     warpgroup is busy;
+//     warpgroup is busy; commits free K_j after S1_j and V_j after PV1_j;
 //   * warps 4-7 / 8-11: softmax warpgroups for Q0 / Q1, ONE THREAD PER QUERY
-//     ROW (32x32b TMEM loads give each thread its own row: no shuffles);
-//     P = exp2(S*scale*log2e - m) is written back as packed 16-bit INTO THE
-//     S COLUMNS OF TMEM and consumed from there (tcgen05.mma, A in TMEM);
-//   * the ROW SUM IS COMPUTED BY THE TENSOR CORE: the P.V MMA multiplies by
-//     [V | 1] (N = D + 16; a constant chunk of ones sits after V in every
-//     ring stage), so the accumulator carries l next to O, rescaled with it
-//     - the softmax threads only do FFMA + EX2 + pack per score, which keeps
-//     the SFU and FMA pipes under the tensor-core time per tile;
+//     ROW (32x32b TMEM loads give each thread its own row: no shuffles).
+//     x = s*scale*log2e - m with packed FFMA2; 2^x on the SFU for most score
+//     pairs and as a Cody-Waite + cubic polynomial on the FMA pipe (FFMA2)
+//     for NTB_ATTN_POLY_PAIRS of every 16 pairs - the SFU alone would need
+//     the whole tensor-core time per tile; row sums in fp32 by FADD2.  P is
+//     written back as packed 16-bit INTO THE S COLUMNS OF TMEM and consumed
+//     from there (tcgen05.mma, A operand in TMEM);
 //   * lazy rescaling: the running max only moves when a row max grows by
-//     more than 2^8; only then is the [O | l] row (TMEM) rescaled.  S_{g,j}
-//     is issued after PV_{g,j-1}, so waiting for S_{g,j} already means the
-//     accumulator is current.
-// TMEM (512 cols): S0/P0 [0,112) S1/P1 [112,224) then [O|l]0, [O|l]1.
+//     more than 2^8; only then is the O row (TMEM) rescaled.  S_{g,j} is
+//     issued after PV_{g,j-1}, so waiting for S_{g,j} means O is current;
+//   * epilogue per item: O row -> registers, O released to the MMA warp
+//     (o_empty) before the normalise-and-store, so the next item's PV can
+//     start while the rows are written.
+// TMEM (512 cols): S0/P0 [0,128) S1/P1 [128,256) O0 [256,256+D) O1 after.
 // Keys beyond S_k are masked to -inf; query rows beyond S_q are not stored.
 // Tensor roofline: 4*B*H*S_q*S_k*D flop per launch.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+
+#include <stdio.h>
 
 #include "common.cuh"
 #include "k_sm100.cuh"
@@ -36,16 +41,35 @@
 namespace ntb {
 namespace {
 
-constexpr int BM = 128, BN = 112;  // query rows per tile, keys per KV tile
+constexpr int BM = 128, BN = 128;  // query rows per tile, keys per KV tile
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+#ifndef NTB_ATTN_POLY_PAIRS
+#define NTB_ATTN_POLY_PAIRS 3  // of every 16 score pairs, 2^x on the FMA pipe
+#endif
+
+#ifndef NTB_ATTN_TRACE
+#define NTB_ATTN_TRACE 0  // debug builds: per-phase clock64 stamps of CTA 0's first item
+#endif
+#if NTB_ATTN_TRACE
+__device__ long long g_attn_trace[2 * 64 * 8 + 64 * 8];
+#define TRACE_SM(g, j, k)                                                          \
+  if (blockIdx.x == 0 && it == 0 && lane == 0 && quad == 0 && (j) < 64)            \
+    g_attn_trace[((g) * 64 + (j)) * 8 + (k)] = clock64();
+#define TRACE_MMA(j, k) \
+  if (blockIdx.x == 0 && it == 0 && (j) < 64) g_attn_trace[128 * 8 + (j) * 8 + (k)] = clock64();
+#else
+#define TRACE_SM(g, j, k)
+#define TRACE_MMA(j, k)
+#endif
 
 struct AttnMaps {
   CUtensorMap q, k, v;
 };
 
 struct AttnParams {
-  int B, H, Sq, Sk;
+  int B, H, Sq, Sk, n_qt, n_items;
   float scale_log2;
   void* o;
   int64_t os[4];
@@ -54,17 +78,16 @@ struct AttnParams {
 template <int D>
 struct Layout {
   static constexpr int DCH = D / 64;               // 128B chunks along D
-  static constexpr int NO = D + 16;                // [O | l] accumulator width
   static constexpr int Q_BYTES = BM * D * 2;       // one query tile
-  static constexpr int KCH = BN * 128;             // one 64-wide chunk of a K/V tile
-  static constexpr int K_BYTES = DCH * KCH;
-  static constexpr int V_BYTES = (DCH + 1) * KCH;  // V chunks + the ones chunk
-  static constexpr int ST_BYTES = K_BYTES + V_BYTES;
+  static constexpr int CH = BN * 128;              // one 64-wide chunk of a K/V tile
+  static constexpr int SLOT = DCH * CH;            // one K or V tile
+  static constexpr int NS = D == 128 ? 5 : 8;      // K/V ring entries
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = 2 * Q_BYTES;
-  static constexpr int SMEM = OFF_KV + 2 * ST_BYTES + 1024;
-  static constexpr uint32_t T_S0 = 0, T_S1 = BN, T_O0 = 2 * BN, T_O1 = 2 * BN + NO;
-  static_assert(2 * BN + 2 * NO <= 512, "TMEM budget");
+  static constexpr int SMEM = OFF_KV + NS * SLOT + 1024;
+  static constexpr uint32_t T_S0 = 0, T_S1 = BN, T_O0 = 2 * BN, T_O1 = 2 * BN + D;
+  static_assert(2 * BN + 2 * D <= 512, "TMEM budget");
+  static_assert(SMEM <= 227 * 1024 - 512, "shared memory budget");
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -73,21 +96,23 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA/ALU pipes (Cody-Waite split + cubic, rel. err 7.5e-5 <
-// half an fp16 ulp): takes a quarter of the exponentials off the SFU, which
-// otherwise needs ~94% of the tensor-core time per KV tile (FA4's trick).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -125.f);
-  const float t = x + 12582912.0f;                    // 1.5 * 2^23: round to int
-  const int i = __float_as_int(t) - 0x4B400000;
-  const float f = x - (t - 12582912.0f);             // f in [-0.5, 0.5]
-  const float q = fmaf(fmaf(fmaf(0.0551702793f, f, 0.242607975f), f, 0.693260928f), f, 0.999928276f);
-  return __int_as_float(__float_as_int(q) + (i << 23));
+// 2^x for a pair on the FMA pipe: x clamped to [-127, .], x = i + f with
+// i = rint(x) (1.5*2^23 trick), f in [-0.5, 0.5]; 2^f by a cubic (rel. err
+// 7.5e-5, below half an fp16 / bf16 ulp); 2^i added into the exponent.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
+  float2 q = __ffma2_rn(f, make_float2(0.0551702793f, 0.0551702793f),
+                        make_float2(0.242607975f, 0.242607975f));
+  q = __ffma2_rn(q, f, make_float2(0.693260928f, 0.693260928f));
+  q = __ffma2_rn(q, f, make_float2(0.999928276f, 0.999928276f));
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
 }
-
-#ifndef NTB_ATTN_POLY
-#define NTB_ATTN_POLY 0  // measured: no gain on B200 (8.05-8.30 ms either way, within noise)
-#endif
 
 template <bool BF16>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -102,33 +127,26 @@ __global__ void __launch_bounds__(384, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full[2],
-      o_full[2];
+  __shared__ __align__(8) uint64_t q_full, q_empty, kv_full[L::NS], kv_empty[L::NS], s_full[2],
+      p_full[2][2], o_full[2], o_empty[2];
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int n_kv = (p.Sk + BN - 1) / BN;
 
-  // constant "ones" chunk after V in both ring stages (row-sum operand)
-  {
-    const uint16_t one = BF16 ? 0x3F80 : 0x3C00;
-    const uint32_t w = one | ((uint32_t)one << 16);
-    for (int st = 0; st < 2; ++st) {
-      uint4* dst = reinterpret_cast<uint4*>(smem + L::OFF_KV + st * L::ST_BYTES + L::K_BYTES +
-                                            L::DCH * L::KCH);
-      for (int i = threadIdx.x; i < L::KCH / 16; i += blockDim.x) dst[i] = make_uint4(w, w, w, w);
-    }
-    fence_proxy_async();
-  }
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    mbar_init(&q_empty, 1);
+    for (int i = 0; i < L::NS; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
-      mbar_init(&o_full[i], 1);
+    }
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&s_full[g], 1);
+      mbar_init(&p_full[g][0], 4);
+      mbar_init(&p_full[g][1], 4);
+      mbar_init(&o_full[g], 1);
+      mbar_init(&o_empty[g], 4);
     }
     fence_barrier_init();
   }
@@ -139,194 +157,269 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-
+  // registers: the producer / MMA warpgroup gives its share to the softmax
+  // warpgroups (one 128-column S row per thread lives in registers)
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
   if (warp == 0) {
     if (elect_one()) {
       tma_prefetch(&maps.q);
       tma_prefetch(&maps.k);
       tma_prefetch(&maps.v);
-      mbar_expect_tx(&q_full, 2 * L::Q_BYTES);
+      uint32_t c = 0;  // K/V ring sequence number: K_j, V_j, K_{j+1}, ...
+      int it = 0;
+      for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+        const int qt = item % p.n_qt, bh = item / p.n_qt, h = bh % p.H, b = bh / p.H;
+        mbar_wait(&q_empty, (it & 1) ^ 1);
+        mbar_expect_tx(&q_full, 2 * L::Q_BYTES);
 #pragma unroll
-      for (int g = 0; g < 2; ++g)
+        for (int g = 0; g < 2; ++g)
 #pragma unroll
-        for (int c = 0; c < L::DCH; ++c)
-          tma_load_4d(smem + L::OFF_Q + g * L::Q_BYTES + c * (BM * 128), &maps.q, &q_full,
-                      c * 64, qt * 2 * BM + g * BM, h, b);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&kv_empty[st], ph ^ 1);
-        mbar_expect_tx(&kv_full[st], L::K_BYTES + L::DCH * L::KCH);
-        uint8_t* kdst = smem + L::OFF_KV + st * L::ST_BYTES;
-        uint8_t* vdst = kdst + L::K_BYTES;
+          for (int ch = 0; ch < L::DCH; ++ch)
+            tma_load_4d(smem + L::OFF_Q + g * L::Q_BYTES + ch * (BM * 128), &maps.q, &q_full,
+                        ch * 64, qt * 2 * BM + g * BM, h, b);
+        for (int j = 0; j < n_kv; ++j) {
 #pragma unroll
-        for (int c = 0; c < L::DCH; ++c) {
-          tma_load_4d(kdst + c * L::KCH, &maps.k, &kv_full[st], c * 64, j * BN, h, b);
-          tma_load_4d(vdst + c * L::KCH, &maps.v, &kv_full[st], c * 64, j * BN, h, b);
+          for (int kv = 0; kv < 2; ++kv, ++c) {
+            const uint32_t slot = c % L::NS;
+            mbar_wait(&kv_empty[slot], ((c / L::NS) & 1) ^ 1);
+            mbar_expect_tx(&kv_full[slot], L::SLOT);
+            uint8_t* dst = smem + L::OFF_KV + slot * L::SLOT;
+#pragma unroll
+            for (int ch = 0; ch < L::DCH; ++ch)
+              tma_load_4d(dst + ch * L::CH, kv ? &maps.v : &maps.k, &kv_full[slot], ch * 64, j * BN,
+                          h, b);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (elect_one()) {
       constexpr uint32_t idesc_s = idesc_f16(BF16, false, false, BM, BN);
-      constexpr uint32_t idesc_o = idesc_f16(BF16, false, true, BM, L::NO);
-      mbar_wait(&q_full, 0);
-      auto issue_s = [&](int g, int j) {
-        const int st = j & 1;
+      constexpr uint32_t idesc_o = idesc_f16(BF16, false, true, BM, D);
+      uint32_t c = 0;  // ring sequence number of K_0 of the current item
+      uint32_t t = 0;  // tiles consumed (p_full phase)
+      int it = 0;
+      auto slot_addr = [&](uint32_t seq) {
+        return smem_u32(smem + L::OFF_KV + (seq % L::NS) * L::SLOT);
+      };
+      auto wait_kv = [&](uint32_t seq) {
+        mbar_wait(&kv_full[seq % L::NS], (seq / L::NS) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](int g, uint32_t kseq) {
         const uint32_t q_addr = smem_u32(smem + L::OFF_Q + g * L::Q_BYTES);
-        const uint32_t k_addr = smem_u32(smem + L::OFF_KV + st * L::ST_BYTES);
+        const uint32_t k_addr = slot_addr(kseq);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-          const uint32_t koff = (kk >> 2) * L::KCH + (kk & 3) * 32;
+          const uint32_t koff = (kk >> 2) * L::CH + (kk & 3) * 32;
           mma_f16_ss(tmem + (g ? L::T_S1 : L::T_S0), umma_desc_sw128(q_addr + off, 16, 1024),
                      umma_desc_sw128(k_addr + koff, 16, 1024), idesc_s, kk != 0);
         }
         mma_commit(&s_full[g]);
       };
-      auto issue_pv = [&](int g, int j) {
-        const int st = j & 1;
-        const uint32_t v_addr = smem_u32(smem + L::OFF_KV + st * L::ST_BYTES + L::K_BYTES);
+      // P.V for one half of the keys (P is released by the softmax in halves)
+      auto issue_pv = [&](int g, uint32_t vseq, bool first, int half) {
+        const uint32_t v_addr = slot_addr(vseq);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
+        for (int k2 = 0; k2 < BN / 32; ++k2) {
+          const int kk = half * (BN / 32) + k2;
           mma_f16_ts(tmem + (g ? L::T_O1 : L::T_O0), tmem + (g ? L::T_S1 : L::T_S0) + kk * 8,
-                     umma_desc_sw128(v_addr + kk * 2048, L::KCH, 1024), idesc_o, (j | kk) != 0);
-      };
-      mbar_wait(&kv_full[0], 0);
-      tc_fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        const bool more = j + 1 < n_kv;
-        mbar_wait(&p_full[0], j & 1);
-        tc_fence_after();
-        issue_pv(0, j);
-        if (more) {
-          mbar_wait(&kv_full[st ^ 1], ((j + 1) >> 1) & 1);   // K/V_{j+1} landed
-          tc_fence_after();
-          issue_s(0, j + 1);
-        } else {
-          mma_commit(&o_full[0]);
+                     umma_desc_sw128(v_addr + kk * 2048, L::CH, 1024), idesc_o,
+                     !(first && kk == 0));
         }
-        mbar_wait(&p_full[1], j & 1);
+      };
+      for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+        mbar_wait(&q_full, it & 1);
         tc_fence_after();
-        issue_pv(1, j);
-        mma_commit(&kv_empty[st]);
-        if (more) issue_s(1, j + 1);
-        else mma_commit(&o_full[1]);
+        wait_kv(c);
+        issue_s(0, c);
+        issue_s(1, c);
+        mma_commit(&kv_empty[c % L::NS]);
+        if (n_kv == 1) mma_commit(&q_empty);
+        for (int j = 0; j < n_kv; ++j, ++t) {
+          const bool more = j + 1 < n_kv;
+          const uint32_t kseq = c + 2 * j, vseq = kseq + 1, knext = kseq + 2;
+          // ---- query tile 0
+          TRACE_MMA(j, 0)
+          mbar_wait(&p_full[0][0], t & 1);
+          tc_fence_after();
+          TRACE_MMA(j, 1)
+          if (j == 0 && it > 0) {
+            mbar_wait(&o_empty[0], (it - 1) & 1);
+            tc_fence_after();
+          }
+          wait_kv(vseq);
+          issue_pv(0, vseq, j == 0, 0);
+          mbar_wait(&p_full[0][1], t & 1);
+          tc_fence_after();
+          TRACE_MMA(j, 2)
+          issue_pv(0, vseq, j == 0, 1);
+          if (more) {
+            wait_kv(knext);
+            TRACE_MMA(j, 3)
+            issue_s(0, knext);
+          } else {
+            mma_commit(&o_full[0]);
+          }
+          // ---- query tile 1
+          TRACE_MMA(j, 4)
+          mbar_wait(&p_full[1][0], t & 1);
+          tc_fence_after();
+          TRACE_MMA(j, 5)
+          if (j == 0 && it > 0) {
+            mbar_wait(&o_empty[1], (it - 1) & 1);
+            tc_fence_after();
+          }
+          issue_pv(1, vseq, j == 0, 0);
+          mbar_wait(&p_full[1][1], t & 1);
+          tc_fence_after();
+          issue_pv(1, vseq, j == 0, 1);
+          mma_commit(&kv_empty[vseq % L::NS]);
+          if (more) {
+            issue_s(1, knext);
+            mma_commit(&kv_empty[knext % L::NS]);
+            if (j + 2 == n_kv) mma_commit(&q_empty);
+          } else {
+            mma_commit(&o_full[1]);
+          }
+          TRACE_MMA(j, 6)
+        }
+        c += 2 * n_kv;
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
     const int g = (warp - 4) >> 2;          // query tile of this warpgroup
     const int quad = warp & 3;              // TMEM lane quadrant
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t t_s = tmem + (g ? L::T_S1 : L::T_S0) + lane_off;
     const uint32_t t_o = tmem + (g ? L::T_O1 : L::T_O0) + lane_off;
-    float m_used = -INFINITY;
-    for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(&s_full[g], j & 1);
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+    uint32_t t = 0;
+    int it = 0;
+    for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+      const int qt = item % p.n_qt, bh = item / p.n_qt, h = bh % p.H, b = bh / p.H;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_kv; ++j, ++t) {
+        TRACE_SM(g, j, 0)
+        mbar_wait(&s_full[g], t & 1);
+        tc_fence_after();
+        TRACE_SM(g, j, 1)
+        const int kvalid = p.Sk - j * BN;
+        uint32_t v[BN];
+#pragma unroll
+        for (int ch = 0; ch < BN / 32; ++ch) tmem_ld_32x32b_x32(t_s + ch * 32, v + ch * 32);
+        tmem_ld_wait();
+        TRACE_SM(g, j, 2)
+        if (kvalid < BN) {
+#pragma unroll
+          for (int i = 0; i < BN; ++i)
+            if (i >= kvalid) v[i] = 0xFF800000u;   // -inf: masked key
+        }
+        // row max: 8 independent chains (a single FMNMX chain is ~64 dependent ops)
+        float mx8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mx8[u] = __uint_as_float(v[u]);
+#pragma unroll
+        for (int i = 8; i < BN; i += 8)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], __uint_as_float(v[i + u]));
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        const float cand = mx * p.scale_log2;
+        const bool warp_grow = __any_sync(0xffffffffu, cand > m_used + kRescaleThreshold);
+        float alpha = 1.f, m_new = m_used;
+        if (warp_grow) {
+          m_new = fmaxf(m_used, cand);
+          alpha = ex2(m_used - m_new);
+          if (j > 0) {
+            // rescale the O row before any of P_j is released (O is current:
+            // S_{g,j} was issued after PV_{g,j-1})
+#pragma unroll
+            for (int ch = 0; ch < D / 32; ++ch) {
+              uint32_t w[32];
+              tmem_ld_32x32b_x32(t_o + ch * 32, w);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(__uint_as_float(w[i]) * alpha);
+              tmem_st_32x32b_x32(t_o + ch * 32, w);
+            }
+          }
+        }
+        TRACE_SM(g, j, 3)
+        const float2 nm2 = make_float2(-m_new, -m_new);
+        float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+#pragma unroll
+          for (int c2 = 0; c2 < BN / 64; ++c2) {
+            const int ch = half * (BN / 64) + c2;
+            uint32_t pk[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const int i = ch * 32 + 2 * q;
+              const float2 x = __ffma2_rn(
+                  make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sc2, nm2);
+              float2 e;
+              if (((q * NTB_ATTN_POLY_PAIRS) % 16) < NTB_ATTN_POLY_PAIRS) {
+                e = ex2_poly2(x);
+              } else {
+                e.x = ex2(x.x);
+                e.y = ex2(x.y);
+              }
+              sum2[q & 1] = __fadd2_rn(sum2[q & 1], e);
+              pk[q] = pack2<BF16>(e.x, e.y);
+            }
+            tmem_st_32x32b_x16(t_s + ch * 16, pk);
+          }
+          // release this half of P_j to the MMA warp
+          if (half == 1) { TRACE_SM(g, j, 6) }
+          tmem_st_wait();
+          if (half == 1) { TRACE_SM(g, j, 7) }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[g][half]);
+          if (half == 0) { TRACE_SM(g, j, 4) }
+        }
+        l = fmaf(l, alpha, (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
+        m_used = m_new;
+        TRACE_SM(g, j, 5)
+      }
+      // epilogue: O row -> registers, release O, then O / l -> global
+      mbar_wait(&o_full[g], it & 1);
       tc_fence_after();
-      const int kvalid = p.Sk - j * BN;
-      // pass 1: row max (S row in registers: 3 x 32 + 16 columns)
-      uint32_t v[BN];
-      tmem_ld_32x32b_x32(t_s, v);
-      tmem_ld_32x32b_x32(t_s + 32, v + 32);
-      tmem_ld_32x32b_x32(t_s + 64, v + 64);
-      tmem_ld_32x32b_x16(t_s + 96, v + 96);
+      uint32_t o[D];
+#pragma unroll
+      for (int ch = 0; ch < D / 32; ++ch) tmem_ld_32x32b_x32(t_o + ch * 32, o + ch * 32);
       tmem_ld_wait();
-      float mx = -INFINITY;
-      if (kvalid >= BN) {
-#pragma unroll
-        for (int i = 0; i < BN; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
-      } else {
-#pragma unroll
-        for (int i = 0; i < BN; ++i)
-          if (i < kvalid) mx = fmaxf(mx, __uint_as_float(v[i]));
-      }
-      const float cand = mx * p.scale_log2;
-      const bool warp_grow = __any_sync(0xffffffffu, cand > m_used + kRescaleThreshold);
-      float alpha = 1.f, m_new = m_used;
-      if (warp_grow) {
-        m_new = fmaxf(m_used, cand);
-        alpha = ex2(m_used - m_new);
-      }
-      // pass 2: P = exp2(s*scale - m), packed into the S columns (in order)
-#pragma unroll
-      for (int c = 0; c < BN / 16; ++c) {
-        uint32_t pk[8];
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const float x0 = fmaf(__uint_as_float(v[c * 16 + i]), p.scale_log2, -m_new);
-          const float x1 = fmaf(__uint_as_float(v[c * 16 + i + 1]), p.scale_log2, -m_new);
-          float e0, e1;
-          if (NTB_ATTN_POLY && (i & 6) == 0) {   // 4 of every 16 scores on the FMA pipe
-            e0 = ex2_poly(x0);
-            e1 = ex2_poly(x1);
-          } else {
-            e0 = ex2(x0);
-            e1 = ex2(x1);
-          }
-          if (kvalid < BN) {
-            if (c * 16 + i >= kvalid) e0 = 0.f;
-            if (c * 16 + i + 1 >= kvalid) e1 = 0.f;
-          }
-          pk[i / 2] = pack2<BF16>(e0, e1);
-        }
-        tmem_st_32x32b_x8(t_s + c * 8, pk);
-      }
-      if (warp_grow && j > 0) {
-        // rescale the [O | l] row (current: S_{g,j} was issued after PV_{g,j-1})
-#pragma unroll
-        for (int c = 0; c < L::NO / 16; ++c) {
-          uint32_t w[16];
-          tmem_ld_32x32b_x16(t_o + c * 16, w);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) w[i] = __float_as_uint(__uint_as_float(w[i]) * alpha);
-          tmem_st_32x32b_x16(t_o + c * 16, w);
-        }
-      }
-      m_used = m_new;
-      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[g]);
-    }
-    // epilogue: O / l -> global (l = accumulator column D)
-    mbar_wait(&o_full[g], 0);
-    tc_fence_after();
-    uint32_t lw[1];
-    tmem_ld_32x32b_x1(t_o + D, lw);
-    tmem_ld_wait();
-    const float inv = 1.f / __uint_as_float(lw[0]);
-    const int qrow = qt * 2 * BM + g * BM + row;
-    char* obase = reinterpret_cast<char*>(p.o) +
-                  ((int64_t)b * p.os[0] + (int64_t)h * p.os[1] + (int64_t)qrow * p.os[2]) * 2;
-    const bool vec = p.os[3] == 1 && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0);
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t w[32];
-      tmem_ld_32x32b_x32(t_o + c * 32, w);
-      tmem_ld_wait();
+      if (lane == 0) mbar_arrive(&o_empty[g]);
+      const float inv = 1.f / l;
+      const int qrow = qt * 2 * BM + g * BM + row;
       if (qrow < p.Sq) {
-        if (vec) {
-          uint4* dst = reinterpret_cast<uint4*>(obase + c * 64);
+        char* obase = reinterpret_cast<char*>(p.o) +
+                      ((int64_t)b * p.os[0] + (int64_t)h * p.os[1] + (int64_t)qrow * p.os[2]) * 2;
+        if (p.os[3] == 1 && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0)) {
+          uint4* dst = reinterpret_cast<uint4*>(obase);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < D / 8; ++u) {
             uint32_t q4[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              q4[e] = pack2<BF16>(__uint_as_float(w[u * 8 + e * 2]) * inv,
-                                  __uint_as_float(w[u * 8 + e * 2 + 1]) * inv);
+              q4[e] = pack2<BF16>(__uint_as_float(o[u * 8 + e * 2]) * inv,
+                                  __uint_as_float(o[u * 8 + e * 2 + 1]) * inv);
             dst[u] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float f = __uint_as_float(w[i]) * inv;
-            const int64_t off = (int64_t)(c * 32 + i) * p.os[3] * 2;
+          for (int i = 0; i < D; ++i) {
+            const float f = __uint_as_float(o[i]) * inv;
+            const int64_t off = (int64_t)i * p.os[3] * 2;
             if constexpr (BF16)
               *reinterpret_cast<__nv_bfloat16*>(obase + off) = __float2bfloat16_rn(f);
             else
@@ -353,8 +446,27 @@ int launch_attn(const AttnMaps& maps, const AttnParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return cuda_fail(e, "attention smem attribute");
     attr_set = true;
   }
-  dim3 grid((unsigned)((p.Sq + 2 * BM - 1) / (2 * BM)), (unsigned)p.H, (unsigned)p.B);
+  const int grid = p.n_items < sm_count() ? p.n_items : sm_count();
   k<<<grid, 384, L::SMEM, s>>>(maps, p);
+#if NTB_ATTN_TRACE
+  {
+    static long long h[2 * 64 * 8 + 64 * 8];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, g_attn_trace, sizeof(h));
+    const long long t0 = h[1 * 8 + 0] ? h[0] : h[0];
+    for (int j = 0; j < 40; ++j) {
+      fprintf(stderr, "j=%2d", j);
+      for (int g = 0; g < 2; ++g) {
+        const long long* r = h + (g * 64 + j) * 8;
+        fprintf(stderr, " | g%d wait@%7lld +%5lld ld %4lld max %4lld h0 %4lld h1c %4lld st %4lld fin %4lld", g,
+                r[0] - t0, r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], r[6] - r[4], r[7] - r[6], r[5] - r[7]);
+      }
+      const long long* m = h + 128 * 8 + j * 8;
+      fprintf(stderr, " | mma p0@%7lld h0 +%4lld h1 +%4lld kv +%4lld p1@ +%4lld h0 +%4lld done +%4lld\n",
+              m[0] - t0, m[1] - m[0], m[2] - m[1], m[3] - m[2], m[4] - m[3], m[5] - m[4], m[6] - m[5]);
+    }
+  }
+#endif
   return check_launch("sdpa tcgen05", NTB_PATH_ATTN_TC);
 }
 
@@ -404,6 +516,9 @@ int attn_sm100(const AttnDesc& a, int dtype, cudaStream_t s) {
   p.H = (int)a.H;
   p.Sq = (int)a.Sq;
   p.Sk = (int)a.Sk;
+  p.n_qt = (int)((a.Sq + 2 * BM - 1) / (2 * BM));
+  if ((int64_t)p.n_qt * a.H * a.B >= (1LL << 31)) return NTB_ERR_UNSUPPORTED;
+  p.n_items = p.n_qt * p.H * p.B;
   p.scale_log2 = a.scale * kLog2e;
   p.o = a.o;
   for (int i = 0; i < 4; ++i) p.os[i] = a.os[i];

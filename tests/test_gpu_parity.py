@@ -256,7 +256,7 @@ def test_conv2d_half(dtype, shape):
 
 @pytest.mark.parametrize("dtype", DTS)
 @pytest.mark.parametrize("bhsd", [(1, 2, 64, 64), (2, 3, 200, 128), (1, 2, 1024, 128),
-                                  (2, 2, 333, 64)])
+                                  (2, 2, 333, 64), (4, 40, 520, 128)])
 def test_sdpa_half(dtype, bhsd):
     b, h, s, d = bhsd
     rng = np.random.default_rng(s)
@@ -267,6 +267,22 @@ def test_sdpa_half(dtype, bhsd):
                    {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128}, dtype,
                    out=torch.zeros((b, h, s, d), device=DEV, dtype=dtype))
     assert pc.delta["attn_tc"] == 1
+    _close(got, oracle.sdpa(q, k, v), rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_sdpa_peaky_scores_rescale(d):
+    """Scores spanning > 2^8 between KV tiles (the lazy O rescale path) and
+    more work items than SMs (persistent CTAs carry barrier phases across
+    items)."""
+    rng = np.random.default_rng(11)
+    b, h, s = 3, 64, 700
+    q = _r16((rng.standard_normal((b, h, s, d)) * 3).astype(np.float32), torch.float16)
+    k = _r16((rng.standard_normal((b, h, s, d)) * 3).astype(np.float32), torch.float16)
+    v = _r16(rng.uniform(-1, 1, (b, h, s, d)).astype(np.float32), torch.float16)
+    got = _run("sdpa", {"q": q, "k": k, "v": v, "o": None},
+               {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128}, torch.float16,
+               out=torch.zeros((b, h, s, d), device=DEV, dtype=torch.float16))
     _close(got, oracle.sdpa(q, k, v), rtol=1e-2, atol=1e-2)
 
 
