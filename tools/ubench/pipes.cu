@@ -19,12 +19,14 @@ __global__ void k(float* out, long long* cyc, float seed) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (OP == 0) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
-      if (OP == 1) { uint32_t r; asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[i]), "f"(a[(i+1)&7])); u[i] ^= r; }
+      if (OP == 1) { asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(u[i]) : "f"(a[i]), "f"(__uint_as_float(u[i]))); }
       if (OP == 2) b[i] = __ffma2_rn(b[i], b[(i + 1) & 7], b[i]);
       if (OP == 3) asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(a[i]));
       if (OP == 4) asm volatile("max.f32 %0, %0, %1;" : "+f"(a[i]) : "f"(a[(i+3)&7]));
-      if (OP == 5) { uint32_t r; asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[i]), "f"(a[(i+1)&7])); u[i] ^= r; }
-      if (OP == 6) { asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i])); uint32_t r; asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[(i+2)&7]), "f"(a[(i+1)&7])); u[i] ^= r; }
+      if (OP == 5) { asm volatile("shl.b32 %0, %0, 3;" : "+r"(u[i])); }
+      if (OP == 6) { asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i])); asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(u[i]) : "f"(a[i]), "f"(__uint_as_float(u[i]))); }
+      if (OP == 7) { asm volatile("add.s32 %0, %0, %1;" : "+r"(u[i]) : "r"(u[(i+1)&7])); }
+      if (OP == 8) { asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(u[i]) : "f"(a[i]), "f"(__uint_as_float(u[i]))); asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(a[i])); }
     }
   }
   long long t1 = clock64();
@@ -38,8 +40,8 @@ int main() {
   float* out; long long* cyc;
   cudaMalloc(&out, 148 * 1024 * 4);
   cudaMalloc(&cyc, 148 * 8);
-  const char* names[] = {"MUFU.EX2", "F2FP f16x2", "FFMA2", "FFMA", "FMNMX", "F2FP bf16x2", "EX2+F2FP"};
-  for (int op = 0; op < 7; ++op) {
+  const char* names[] = {"MUFU.EX2", "F2FP f16x2", "FFMA2", "FFMA", "FMNMX", "SHL", "EX2+F2FP", "IADD", "F2FP+FFMA"};
+  for (int op = 0; op < 9; ++op) {
     for (int wps = 1; wps <= 4; wps *= 2) {
       int threads = 128 * wps;
       for (int rep = 0; rep < 2; ++rep) {
@@ -51,6 +53,8 @@ int main() {
           case 4: k<4><<<148, threads>>>(out, cyc, 0.1f); break;
           case 5: k<5><<<148, threads>>>(out, cyc, 0.1f); break;
           case 6: k<6><<<148, threads>>>(out, cyc, 0.1f); break;
+          case 7: k<7><<<148, threads>>>(out, cyc, 0.1f); break;
+          case 8: k<8><<<148, threads>>>(out, cyc, 0.1f); break;
         }
       }
       long long c;
