@@ -67,7 +67,7 @@ constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
 constexpr int TMEM_COLS = 512;         // 2 accumulators x 256 fp32 columns
 
 struct GemmMaps {
-  CUtensorMap a, b;
+  CUtensorMap a, b, c;   // c: output, box {64 cols, 32 rows, 1}, 128B swizzle (TMA-store epilogue)
 };
 
 struct GemmParams {
@@ -78,6 +78,7 @@ struct GemmParams {
   int64_t d_m, d_n, d_sm, d_sn;
   float alpha, beta;
   int has_d;
+  int tma_c;   // output written by TMA stores from a swizzled smem staging tile
 };
 
 template <bool BF16>
@@ -332,7 +333,102 @@ constexpr int PSTAGES = 6;
 constexpr int PA_BYTES = 128 * BK * 2;
 constexpr int PB_BYTES = 128 * BK * 2;
 constexpr int PSTAGE_BYTES = PA_BYTES + PB_BYTES;
-constexpr int PSMEM_BYTES = PSTAGES * PSTAGE_BYTES + 1024;
+constexpr int PSTAGE_C_BYTES = 4 * 2 * 32 * 128;   // 4 epilogue warps x 2 buffers x 32 rows x 128 B
+constexpr int PSMEM_BYTES = PSTAGES * PSTAGE_BYTES + PSTAGE_C_BYTES + 1024;
+
+// TMA-store epilogue for one warp's 32 accumulator rows of a 256-column
+// tile: 64 columns at a time, fp32 alpha/beta epilogue, packed to 16-bit and
+// written row-per-lane into a 128B-swizzled 32 x 64 staging tile (conflict-
+// free: lanes 8 apart hit the same 16-byte chunk column only after the XOR),
+// then one lane issues a TMA store that clips at the output extent.  Two
+// staging buffers per warp: a buffer is rewritten only after the store that
+// read it has finished reading (bulk wait_group.read).
+template <bool BF16>
+__device__ __forceinline__ void epilogue_tma(const GemmParams& p, const CUtensorMap* cmap,
+                                             uint32_t taddr, uint8_t* stage, int b, int row0,
+                                             int row, int col_base, uint64_t* tempty_leader_bar,
+                                             int lane) {
+  using namespace sm100;
+#pragma unroll 1
+  for (int cc = 0; cc < 4; ++cc) {
+    uint32_t v[64];
+    __syncwarp();
+    tmem_ld_32x32b_x32(taddr + cc * 64, v);
+    tmem_ld_32x32b_x32(taddr + cc * 64 + 32, v + 32);
+    tmem_ld_wait();
+    if (cc == 3) {
+      // the accumulator is in registers: release TMEM to the next tile's MMAs
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_addr(tempty_leader_bar));
+    }
+    const int col0 = col_base + cc * 64;
+    float f[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
+    if (p.has_d && row < p.d_m) {
+      const bool dvec = p.d_sn == 1 && col0 + 64 <= p.d_n && (p.d_sm % 8) == 0 &&
+                        ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0);
+      if (dvec) {
+        const uint4* dp = reinterpret_cast<const uint4*>(
+            reinterpret_cast<const char*>(p.d) + ((int64_t)row * p.d_sm + col0) * 2);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint4 u = dp[q];
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float lo, hi;
+            if constexpr (BF16) {
+              __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[e]);
+              lo = __low2float(h);
+              hi = __high2float(h);
+            } else {
+              __half2 h = *reinterpret_cast<const __half2*>(&w[e]);
+              lo = __low2float(h);
+              hi = __high2float(h);
+            }
+            f[q * 8 + e * 2] += p.beta * lo;
+            f[q * 8 + e * 2 + 1] += p.beta * hi;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const int col = col0 + i;
+          const float dv = col < p.d_n
+                               ? load_el<BF16>(p.d, (int64_t)row * p.d_sm + (int64_t)col * p.d_sn)
+                               : 0.f;
+          f[i] += p.beta * dv;
+        }
+      }
+    }
+    uint8_t* buf = stage + (cc & 1) * (32 * 128);
+    // the store issued from this buffer two chunks ago (possibly in the
+    // previous tile) must have finished reading it
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    const uint32_t base = smem_u32(buf) + lane * 128;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        w[e] = BF16 ? pack_bf16(f[q * 8 + e * 2], f[q * 8 + e * 2 + 1])
+                    : pack_f16(f[q * 8 + e * 2], f[q * 8 + e * 2 + 1]);
+      const uint32_t addr = base + ((q ^ (lane & 7)) << 4);
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]), "r"(w[1]),
+                   "r"(w[2]), "r"(w[3])
+                   : "memory");
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(cmap, buf, col0, row0, b);
+      bulk_commit();
+    }
+  }
+}
 
 template <bool A_MN, bool B_MN, bool BF16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
@@ -343,6 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + PSTAGES * PA_BYTES;
+  uint8_t* sC = smem + PSTAGES * PSTAGE_BYTES;   // epilogue staging (TMA-store path)
   __shared__ __align__(8) uint64_t full[PSTAGES], empty[PSTAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
 
@@ -367,6 +464,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&maps.a);
     tma_prefetch(&maps.b);
+    if (p.tma_c) tma_prefetch(&maps.c);
   }
   if (warp == 2) {
     tmem_alloc_pair(&tmem_slot, TMEM_COLS);
@@ -453,13 +551,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       const uint32_t aph = (tl >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int row = mt * 256 + (int)rank * 128 + ew * 32 + lane;
-      epilogue_row<BF16>(p, tmem_base + acc * 256 + ((uint32_t)(ew * 32) << 16), b, row,
-                         nt * 256);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+      const int row0 = mt * 256 + (int)rank * 128 + ew * 32;
+      const int row = row0 + lane;
+      if (p.tma_c) {
+        epilogue_tma<BF16>(p, &maps.c, tmem_base + acc * 256 + ((uint32_t)(ew * 32) << 16),
+                           sC + ew * (2 * 32 * 128), b, row0, row, nt * 256, &tempty[acc], lane);
+      } else {
+        epilogue_row<BF16>(p, tmem_base + acc * 256 + ((uint32_t)(ew * 32) << 16), b, row,
+                           nt * 256);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+      }
     }
+    if (p.tma_c && lane == 0) bulk_wait<0>();   // all output stores complete before exit
   }
   __syncthreads();
   cluster_sync();
@@ -562,6 +667,15 @@ int gemm_sm100(const GemmDesc& g, int dtype, cudaStream_t s) {
   p.alpha = g.alpha;
   p.beta = g.beta;
   p.has_d = g.d != nullptr;
+  p.tma_c = 0;
+  if (pair && g.c_sn == 1 && aligned16(g.c) && ok_stride(g.c_sm) &&
+      (g.batch == 1 || ok_stride(g.c_sb)) && !getenv("NTB_GEMM_NO_TMA_STORE")) {
+    uint64_t dims[3] = {(uint64_t)g.c_n, (uint64_t)g.c_m, (uint64_t)g.batch};
+    uint64_t str[2] = {(uint64_t)g.c_sm * 2,
+                       g.batch > 1 ? (uint64_t)g.c_sb * 2 : (uint64_t)g.c_m * g.c_sm * 2};
+    uint32_t box[3] = {64, 32, 1};
+    p.tma_c = encode_tmap(&maps.c, dt, 3, g.c, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
   if (pair) {
     p.num_m = (int)cdiv64(g.c_m, 256);
     p.num_n = (int)cdiv64(g.c_n, 256);
