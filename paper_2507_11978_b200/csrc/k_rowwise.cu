@@ -15,8 +15,6 @@
 // the rms_norm weight, L2-resident across rows).
 // Generic path: one CTA per (row, chunk) over arbitrary element strides.
 #include <math.h>
-#include <stdio.h>
-#include <stdlib.h>
 
 #include <type_traits>
 
@@ -111,18 +109,13 @@ __global__ void __launch_bounds__(256) row_vec_kernel(const T* __restrict__ in, 
 
 
 // ---- TMA-bulk row streaming (the B200 fast path) --------------------------
-// Persistent CTAs, one per SM, each owning a contiguous chunk of rows.  The
-// CTA's shared memory is one ring of nw x stages row slots (up to 227 KB):
-// warp w processes local rows w, w + nw, ...; slot (w, k % stages).  One
-// thread issues the first nw x stages rows by cp.async.bulk (global ->
-// shared, completion on the slot's mbarrier) right after the barriers are
-// initialised, so at the BASELINE shape (27-28 rows of 8 KB per SM) the
-// whole chunk is requested at kernel start: every byte the SM will read is
-// in flight at once and the kernel is one DRAM round trip plus the stream.
-// A warp refills its slot with row + nw x stages when it is done with it.
-// The warp reduces its row out of shared memory (warp shuffles, fp32
-// accumulation) and writes the result with 128-bit streaming stores.
-constexpr int kStreamMaxWarps = 32;
+// Persistent CTAs of 8 warps; every warp owns a private ring of S row
+// buffers in shared memory filled by cp.async.bulk (global -> shared, one
+// bulk copy per row, completion on a per-buffer mbarrier), so each SM keeps
+// 8 x (S-1) rows (>= 100 KB) in flight - enough to cover HBM latency at full
+// bandwidth.  The warp reduces its row out of shared memory (warp shuffles,
+// fp32) and writes the result with 128-bit streaming stores.
+constexpr int kStreamWarps = 16;
 constexpr int kStreamMaxStages = 8;
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -223,7 +216,7 @@ __device__ __forceinline__ void rms_row_f16(const uint4* buf, const uint4* wv, _
   const float rinv = 1.0f / sqrtf(warp_sum(ss) / (float)cols + kRmsEps);
   const __half2 r2 = __float2half2_rn(rinv);
   for (int c = lane; c < n_vec; c += 32) {
-    const uint4 v = buf[c], g = ld_keep(wv + c);
+    const uint4 v = buf[c], g = wv[c];
     const uint4 o = make_uint4(h2u(__hmul2(__hmul2(u2h(v.x), r2), u2h(g.x))),
                                h2u(__hmul2(__hmul2(u2h(v.y), r2), u2h(g.y))),
                                h2u(__hmul2(__hmul2(u2h(v.z), r2), u2h(g.z))),
@@ -233,44 +226,47 @@ __device__ __forceinline__ void rms_row_f16(const uint4* buf, const uint4* wv, _
 }
 
 template <typename T, bool kSoftmax>
-__global__ void __launch_bounds__(kStreamMaxWarps * 32, 1)
+__global__ void __launch_bounds__(kStreamWarps * 32, 1)
     row_stream_kernel(const T* __restrict__ in, int64_t in_rs, const T* __restrict__ w,
                       T* __restrict__ out, int64_t out_rs, int64_t rows, int cols, int stages) {
   using P = Pack<T>;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bars[kStreamMaxWarps * kStreamMaxStages];
-  const int nw = blockDim.x >> 5;
+  __shared__ __align__(8) uint64_t bars[kStreamWarps][kStreamMaxStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t row_bytes = (uint32_t)cols * sizeof(T);
   const uint32_t row_pad = (row_bytes + 127u) & ~127u;
-  // contiguous, balanced chunk of rows for this CTA
-  const int64_t base = rows / gridDim.x, extra = rows % gridDim.x;
-  const int64_t r0 = (int64_t)blockIdx.x * base + (blockIdx.x < extra ? blockIdx.x : extra);
-  const int64_t n = base + (blockIdx.x < extra ? 1 : 0);
-  const int64_t ring = (int64_t)nw * stages;
+  uint8_t* wbase = smem + (size_t)warp * stages * row_pad;
+  const T* wsh = nullptr;
   pdl_wait();
   pdl_trigger();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < ring; ++i) bar_init(&bars[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // slot of local row i (< ring): warp i % nw, stage i / nw
-    for (int64_t i = 0; i < n && i < ring; ++i) {
-      const int wi = (int)(i % nw), st = (int)(i / nw);
-      bar_expect(&bars[wi * stages + st], row_bytes);
-      bulk_g2s(smem + (size_t)(wi * stages + st) * row_pad, in + (r0 + i) * in_rs, row_bytes,
-               &bars[wi * stages + st]);
+  if (!kSoftmax) {
+    // weight row once per CTA, after the per-warp rings
+    uint8_t* wdst = smem + (size_t)kStreamWarps * stages * row_pad;
+    for (int c = threadIdx.x; c < cols / P::N; c += blockDim.x)
+      reinterpret_cast<uint4*>(wdst)[c] = reinterpret_cast<const uint4*>(w)[c];
+    wsh = reinterpret_cast<const T*>(wdst);
+  }
+  if (lane == 0)
+    for (int s = 0; s < stages; ++s) bar_init(&bars[warp][s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  const int64_t step = (int64_t)gridDim.x * kStreamWarps;
+  const int64_t first = (int64_t)blockIdx.x * kStreamWarps + warp;
+  if (lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      const int64_t r = first + s * step;
+      if (r < rows) {
+        bar_expect(&bars[warp][s], row_bytes);
+        bulk_g2s(wbase + (size_t)s * row_pad, in + r * in_rs, row_bytes, &bars[warp][s]);
+      }
     }
   }
-  __syncthreads();
-  const T* wsh = w;   // rms_norm weight: read through L1 (one 128-bit pack per lane-step)
-  uint8_t* wbase = smem + (size_t)warp * stages * row_pad;
-  uint64_t* wbars = &bars[warp * stages];
   const int n_vec = cols / P::N;
   int64_t k = 0;
-  for (int64_t i = warp; i < n; i += nw, ++k) {
-    const int64_t r = r0 + i;
+  for (int64_t r = first; r < rows; r += step, ++k) {
     const int s = (int)(k % stages);
-    bar_wait(&wbars[s], (uint32_t)((k / stages) & 1));
+    bar_wait(&bars[warp][s], (uint32_t)((k / stages) & 1));
     const uint4* buf = reinterpret_cast<const uint4*>(wbase + (size_t)s * row_pad);
     T* dst = out + r * out_rs;
     if constexpr (std::is_same<T, __half>::value) {
@@ -334,7 +330,7 @@ __global__ void __launch_bounds__(kStreamMaxWarps * 32, 1)
       for (int c = lane; c < n_vec; c += 32) {
         P v, g;
         v.raw = buf[c];
-        g.raw = ld_keep(wv + c);
+        g.raw = wv[c];
         float f[P::N], gf[P::N];
         v.to_float(f);
         g.to_float(gf);
@@ -348,11 +344,11 @@ __global__ void __launch_bounds__(kStreamMaxWarps * 32, 1)
     // release the buffer: all lanes done reading, then refill it
     __syncwarp();
     if (lane == 0) {
-      const int64_t ni = i + ring;
-      if (ni < n) {
+      const int64_t nr = r + (int64_t)stages * step;
+      if (nr < rows) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bar_expect(&wbars[s], row_bytes);
-        bulk_g2s(wbase + (size_t)s * row_pad, in + (r0 + ni) * in_rs, row_bytes, &wbars[s]);
+        bar_expect(&bars[warp][s], row_bytes);
+        bulk_g2s(wbase + (size_t)s * row_pad, in + nr * in_rs, row_bytes, &bars[warp][s]);
       }
     }
   }
@@ -367,36 +363,11 @@ static bool try_stream(const T* in, int64_t in_rs, const T* w, T* out, int64_t o
       !aligned16(out) || (w && !aligned16(w)) || rows < 1)
     return false;
   const int64_t row_pad = (row_bytes + 127) & ~int64_t(127);
-  const int64_t budget = 227 * 1024 - 2048;   // opt-in max minus static smem
-  const int64_t slots = budget / row_pad;
-  if (slots < 1) return false;
-  const int64_t grid = rows < sm_count() ? rows : sm_count();
-  const int64_t rpc = cdiv64(rows, grid);   // rows of the largest chunk
-  // ring shape: the whole chunk in flight if it fits (with the most warps
-  // that allow it), else the biggest ring with the most warps
-  int nw = 0, stages = 0;
-  for (int w_ = kStreamMaxWarps; w_ >= 4; --w_) {
-    const int64_t st = cdiv64(rpc, w_);
-    if (st <= kStreamMaxStages && w_ * st <= slots) { nw = w_; stages = (int)st; break; }
-  }
-  static const char* force = getenv("NTB_ROW_RING");   // "nw,stages" (tuning sweeps)
-  if (force) {
-    int a = 0, b = 0;
-    if (sscanf(force, "%d,%d", &a, &b) == 2 && a >= 1 && a <= kStreamMaxWarps && b >= 1 &&
-        b <= kStreamMaxStages && a * b <= slots) {
-      nw = a;
-      stages = b;
-    }
-  }
-  if (!nw) {
-    for (int w_ = kStreamMaxWarps; w_ >= 1 && !nw; --w_) {
-      int64_t st = slots / w_;
-      if (st > kStreamMaxStages) st = kStreamMaxStages;
-      if (st >= 2 || (w_ <= 4 && st >= 1)) { nw = w_; stages = (int)st; }
-    }
-    if (!nw) return false;
-  }
-  const size_t smem = (size_t)(nw * stages * row_pad);
+  const int64_t budget = 200 * 1024 - (kSoftmax ? 0 : row_pad);
+  int64_t stages = budget / (kStreamWarps * row_pad);
+  if (stages > kStreamMaxStages) stages = kStreamMaxStages;
+  if (stages < 1) return false;
+  const size_t smem = (size_t)(kStreamWarps * stages * row_pad + (kSoftmax ? 0 : row_pad));
   auto kern = row_stream_kernel<T, kSoftmax>;
   static size_t attr = 0;
   if (smem > attr) {
@@ -405,8 +376,10 @@ static bool try_stream(const T* in, int64_t in_rs, const T* w, T* out, int64_t o
       return false;
     attr = smem;
   }
-  launch_pdl(kern, dim3((unsigned)grid), dim3(nw * 32), smem, s, in, in_rs, w, out, out_rs, rows,
-             (int)cols, stages);
+  int64_t blocks = cdiv64(rows, kStreamWarps);
+  if (blocks > sm_count()) blocks = sm_count();
+  launch_pdl(kern, dim3((unsigned)blocks), dim3(kStreamWarps * 32), smem, s, in, in_rs, w, out,
+             out_rs, rows, (int)cols, (int)stages);
   return true;
 }
 
