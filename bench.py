@@ -255,6 +255,32 @@ def build_works(dev, which):
                          sdpa_setup, lambda a: B.sdpa_launch(a["q"], a["k"], a["v"], a["o"], 128, 128),
                          note="single input set (4.3 GB working set >> L2)")
 
+    def sdpa_rope_setup():
+        shp = (32, 4096, 32, 128)                  # (B, S, H, D) storage, viewed (B, H, S, D)
+        ang = torch.rand((4096, 64), generator=g, device=dev) * 6 - 3
+        return [dict(q=U(shp), k=U(shp), v=U(shp), s=torch.sin(ang).half(), c=torch.cos(ang).half(),
+                     qr=torch.empty(shp, device=dev, dtype=f16),
+                     kr=torch.empty(shp, device=dev, dtype=f16),
+                     o=torch.empty((32, 32, 4096, 128), device=dev, dtype=f16))]
+
+    def T(x):
+        return x.transpose(1, 2)
+
+    works["sdpa_rope"] = Work(
+        "sdpa(rope(q), rope(k), v) fp16 B32 H32 S4096 D128, one fused kernel", "tensor",
+        4 * 32 * 32 * 4096 * 4096 * 128, sdpa_rope_setup,
+        lambda a: B.sdpa_rope_launch(T(a["q"]), T(a["k"]), T(a["v"]), a["s"], a["c"], a["s"], a["c"],
+                                     a["o"], 128, 128),
+        note="q, k, v in the paper's (B, S, H, D) layout viewed as (B, H, S, D); rotary "
+             "embedding applied in shared memory (no rotated copies in HBM)")
+    works["rope+sdpa"] = Work(
+        "rope(q), rope(k), sdpa: the unfused pipeline of sdpa_rope (3 launches)", "tensor",
+        4 * 32 * 32 * 4096 * 4096 * 128, sdpa_rope_setup,
+        lambda a: (B.rope_launch(a["q"], a["s"], a["c"], a["qr"], 64),
+                   B.rope_launch(a["k"], a["s"], a["c"], a["kr"], 64),
+                   B.sdpa_launch(T(a["qr"]), T(a["kr"]), T(a["v"]), a["o"], 128, 128)),
+        note="reference point for sdpa_rope: rotated Q/K round-trip through HBM (4.3 GB)")
+
     def rope_setup():
         shp = (32, 4096, 32, 128)
         ang = torch.rand((4096, 64), generator=g, device=dev) * 6 - 3
@@ -594,7 +620,7 @@ def main():
     h = headline(args, n_gpus, rank, pk)
     kernels = {}
     names = ["add_2^20", "add_2^24", "silu_2^24", "softmax", "rms_norm", "mm", "addmm", "bmm",
-             "conv2d", "sdpa", "rope"]
+             "conv2d", "sdpa", "rope", "sdpa_rope", "rope+sdpa"]
     sel = names if args.kernels == "all" else ([] if args.kernels == "none"
                                                else args.kernels.split(","))
     traffic = ncu_traffic()
@@ -602,7 +628,7 @@ def main():
         works = build_works(torch.device("cuda", local), sel)
         for key, wk in works.items():
             try:
-                steps = args.kernel_steps if wk.bound == "hbm" or key not in ("sdpa",) else 3
+                steps = 3 if key in ("sdpa", "sdpa_rope", "rope+sdpa") else args.kernel_steps
                 ms, total, launches = time_work(wk, steps, 2, n_gpus)
                 ms = _max_over_ranks(ms, n_gpus)
                 kernels[key] = {"workload": wk.name, "ms": round(ms, 5),

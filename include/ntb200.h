@@ -60,7 +60,8 @@ enum {
   NTB_K_ADDMM = 7,    /* catalog.py:260-292 */
   NTB_K_CONV2D = 8,   /* catalog.py:295-330 */
   NTB_K_SDPA = 9,     /* builder-defined (absent upstream, catalog.py:36) */
-  NTB_K_ROPE = 10     /* builder-defined (absent upstream, catalog.py:36) */
+  NTB_K_ROPE = 10,    /* builder-defined (absent upstream, catalog.py:36) */
+  NTB_K_SDPA_ROPE = 11 /* sdpa(rope(q), rope(k), v) in one kernel: SURVEY 8(f) rank 1 */
 };
 
 /* ---- library ----------------------------------------------------------- */

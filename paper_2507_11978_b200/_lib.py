@@ -19,7 +19,7 @@ if os.environ.get("NTB_LIB_VARIANT"):
 NTB_OK, NTB_ERR_ARG, NTB_ERR_CHECK, NTB_ERR_UNSUPPORTED, NTB_ERR_CUDA, NTB_ERR_EVAL = range(6)
 NTB_F32, NTB_F16, NTB_BF16 = 0, 1, 2
 KERNEL_IDS = {"add": 1, "silu": 2, "softmax": 3, "rms_norm": 4, "mm": 5, "bmm": 6,
-              "addmm": 7, "conv2d": 8, "sdpa": 9, "rope": 10}
+              "addmm": 7, "conv2d": 8, "sdpa": 9, "rope": 10, "sdpa_rope": 11}
 
 # every symbol include/ntb200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("ntb_abi_version", "ntb_last_error", "ntb_launch_count", "ntb_path_count",

@@ -14,6 +14,14 @@ builder-defined and documented in DESIGN.md:
 * rope: half-split ("NeoX") rotary embedding of x (B, S, H, D) with
   sin/cos tables (S, D/2): ``y1 = x1*cos - x2*sin``, ``y2 = x1*sin + x2*cos``
   where x1/x2 are the two D/2 halves (PAPER.md:846 signature).
+* sdpa_rope: ``sdpa(rope(q), rope(k), v)`` as ONE kernel (SURVEY 8(f) rank
+  1: the rotated Q/K never go through HBM).  The tile IR has no program-id
+  expression, so the rotary tables enter twice: ``sin_q``/``cos_q`` blocked
+  like the query rows (outer level), ``sin_k``/``cos_k`` blocked like the key
+  rows (nest level); callers pass the same (S, D/2) tables for both.  The
+  rotation is written with two elementwise IR ops: ``rotate_half(x) =
+  [-x2, x1]`` and ``dup2(t) = [t, t]`` along the last axis, so
+  ``rope(x) = x * dup2(cos) + rotate_half(x) * dup2(sin)``.
 """
 
 from __future__ import annotations
@@ -29,7 +37,7 @@ from .symbolic import var
 from .tensor import FULL, new_param
 
 CATALOG_NAMES = ("add", "silu", "softmax", "rms_norm", "mm", "bmm", "addmm", "conv2d")
-EXTRA_NAMES = ("sdpa", "rope")
+EXTRA_NAMES = ("sdpa", "rope", "sdpa_rope")
 ALL_NAMES = CATALOG_NAMES + EXTRA_NAMES
 
 RMS_NORM_EPS = 1e-6
@@ -331,10 +339,79 @@ def spec_rope() -> KernelSpec:
                       body)
 
 
+def _rope_ir(x, c, s):
+    """x * dup2(c) + rotate_half(x) * dup2(s) (half-split rotary embedding)."""
+    return BinOp("+", BinOp("*", x, UnOp("dup2", c)),
+                 BinOp("*", UnOp("rotate_half", x), UnOp("dup2", s)))
+
+
+def spec_sdpa_rope() -> KernelSpec:
+    """Builder-defined sdpa(rope(q), rope(k), v)."""
+    bm, bn = var("BLOCK_SIZE_M"), var("BLOCK_SIZE_N")
+    recs = {}
+    for n in ("q", "o"):
+        r = Rec(n, 4).tile((1, 1, bm, FULL))    # outer (B, H, Mt, 1), inner (1, 1, bm, D)
+        r.squeeze(3)
+        r.flatten(0, 2)                          # outer (B*H, Mt)
+        r.squeeze(0, depth=1)
+        r.squeeze(0, depth=1)                    # inner (bm, D)
+        recs[n] = r
+    bh, m_tiles = recs["o"].shape
+    for n in ("k", "v"):
+        r = Rec(n, 4).tile((1, 1, bn, FULL))
+        r.tile((1, 1, FULL, 1))
+        r.expand((-1, -1, m_tiles, -1))
+        r.squeeze(3)
+        r.flatten(0, 2)                          # outer (B*H, Mt)
+        r.squeeze(0, depth=1)
+        r.squeeze(0, depth=1)
+        r.squeeze(1, depth=1)                    # nest (Nt,)
+        r.squeeze(0, depth=2)
+        r.squeeze(0, depth=2)                    # inner (bn, D)
+        recs[n] = r
+    for n in ("sin_q", "cos_q"):
+        r = Rec(n, 2).tile((bm, FULL))           # outer (Mt, 1), inner (bm, D/2)
+        r.permute((1, 0))
+        r.expand((bh, -1))                       # outer (B*H, Mt)
+        recs[n] = r
+    for n in ("sin_k", "cos_k"):
+        r = Rec(n, 2).tile((bn, FULL))           # outer (Nt, 1), inner (bn, D/2)
+        r.tile((FULL, 1))                        # outer (1, 1), nest (Nt, 1)
+        r.expand((bh, m_tiles))
+        r.squeeze(1, depth=1)                    # nest (Nt,)
+        recs[n] = r
+    d = ShapeOf("q", 3, "source")
+    kj = Load("k", (Var("j"),), float("-inf"))
+    krot = _rope_ir(kj, Load("cos_k", (Var("j"),)), Load("sin_k", (Var("j"),)))
+    body = (
+        Let("qt", _rope_ir(Load("q"), Load("cos_q"), Load("sin_q"))),
+        Let("scale", BinOp("/", ConstF(1.0), UnOp("sqrt", d))),
+        Let("acc", Zeros((bm, var("q_size_3")), "f32")),
+        Let("l", Zeros((bm,), "f32")),
+        Let("m", BinOp("-", Zeros((bm,), "f32"), ConstF(float("inf")))),
+        ForRange("j", ShapeOf("k", 0, "nest"), (
+            Let("s", BinOp("*", Dot(Local("qt"), UnOp("trans", krot)), Local("scale"))),
+            Let("m_new", BinOp("max", Local("m"), Reduce("max", 1, Local("s")))),
+            Let("p", UnOp("exp", BinOp("-", Local("s"), Local("m_new")))),
+            Let("alpha", UnOp("exp", BinOp("-", Local("m"), Local("m_new")))),
+            Assign("l", BinOp("+", BinOp("*", Local("l"), Local("alpha")), Reduce("sum", 1, Local("p")))),
+            Assign("acc", BinOp("+", BinOp("*", Local("acc"), Local("alpha")),
+                                Dot(Local("p"), Load("v", (Var("j"),))))),
+            Assign("m", Local("m_new")),
+        )),
+        Store("o", BinOp("/", Local("acc"), Local("l"))),
+    )
+    names = ("q", "k", "v", "sin_q", "cos_q", "sin_k", "cos_k", "o")
+    params = tuple(ParamSpec(n, 2 if n.startswith(("sin", "cos")) else 4, "f16",
+                             "out" if n == "o" else "in") for n in names)
+    return KernelSpec("sdpa_rope", params, ("BLOCK_SIZE_M", "BLOCK_SIZE_N"),
+                      {n: tuple(recs[n].ops) for n in names}, body)
+
+
 _MAKERS = {
     "add": spec_add, "silu": spec_silu, "softmax": spec_softmax, "rms_norm": spec_rms_norm,
     "mm": spec_mm, "bmm": spec_bmm, "addmm": spec_addmm, "conv2d": spec_conv2d,
-    "sdpa": spec_sdpa, "rope": spec_rope,
+    "sdpa": spec_sdpa, "rope": spec_rope, "sdpa_rope": spec_sdpa_rope,
 }
 
 

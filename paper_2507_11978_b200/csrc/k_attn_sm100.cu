@@ -73,9 +73,86 @@ struct AttnParams {
   float scale_log2;
   void* o;
   int64_t os[4];
+  // rope fusion (sdpa_rope): half-split rotary tables (S, D/2) of the query
+  // rows, row strides in elements
+  const void *sin_q, *cos_q;
+  int64_t sq_rs, cq_rs;
 };
 
-template <int D>
+// Rotate `rows` rows of a 128B-swizzled K-major tile in place (half-split
+// rotary embedding, x0 = columns [0, D/2), x1 = [D/2, D)):
+//   x0' = x0*c - x1*s,  x1' = x0*s + x1*c   (fp32, rounded to 16 bit)
+// with c/s = the table rows of positions pos0 + row.  Thread t of `nthr`
+// takes 16-byte units round-robin; the pair of units (x0, x1) sits at the
+// same swizzled offset of the two 64-column chunks (D = 128) or 64 bytes
+// apart in one chunk (D = 64).  Conflict-free: 8 consecutive rows put the
+// same unit at 8 different 16-byte columns.
+template <int D, bool BF16>
+__device__ __forceinline__ void rope_tile(uint8_t* tile, int chunk_bytes, int rows, int pos0,
+                                          int pos_limit, const void* sn, int64_t sn_rs,
+                                          const void* cs, int64_t cs_rs, int t, int nthr) {
+  constexpr int UPR = D / 16;           // 16-byte units per half row (8 elements each)
+  const uint16_t* sb = reinterpret_cast<const uint16_t*>(sn);
+  const uint16_t* cb = reinterpret_cast<const uint16_t*>(cs);
+  constexpr int BATCH = 4;   // units in flight per thread: table loads come from L2
+  for (int i0 = t; i0 < rows * UPR; i0 += nthr * BATCH) {
+    uint4 x0[BATCH], x1[BATCH], c4[BATCH], s4[BATCH];
+    uint4* p0[BATCH];
+    uint4* p1[BATCH];
+    bool ok[BATCH];
+#pragma unroll
+    for (int k = 0; k < BATCH; ++k) {
+      const int i = i0 + k * nthr;
+      const int r = i / UPR, u = i % UPR;
+      const int pos = pos0 + r;
+      // rows past the sequence are zero (TMA fill) and never stored
+      ok[k] = i < rows * UPR && pos < pos_limit;
+      uint8_t* rowp = tile + r * 128;
+      p0[k] = reinterpret_cast<uint4*>(rowp + ((u ^ (r & 7)) << 4));
+      p1[k] = D == 128 ? reinterpret_cast<uint4*>(rowp + chunk_bytes + ((u ^ (r & 7)) << 4))
+                       : reinterpret_cast<uint4*>(rowp + (((u + 4) ^ (r & 7)) << 4));
+      if (ok[k]) {
+        x0[k] = *p0[k];
+        x1[k] = *p1[k];
+        c4[k] = ld_keep(cb + (int64_t)pos * cs_rs + u * 8);
+        s4[k] = ld_keep(sb + (int64_t)pos * sn_rs + u * 8);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < BATCH; ++k) {
+      if (!ok[k]) continue;
+      const uint32_t a[4] = {x0[k].x, x0[k].y, x0[k].z, x0[k].w};
+      const uint32_t b[4] = {x1[k].x, x1[k].y, x1[k].z, x1[k].w};
+      const uint32_t cc[4] = {c4[k].x, c4[k].y, c4[k].z, c4[k].w};
+      const uint32_t ss[4] = {s4[k].x, s4[k].y, s4[k].z, s4[k].w};
+      uint32_t o0[4], o1[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 fa, fb, fc, fs;
+        if constexpr (BF16) {
+          fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a[e]));
+          fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b[e]));
+          fc = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cc[e]));
+          fs = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ss[e]));
+        } else {
+          fa = __half22float2(*reinterpret_cast<const __half2*>(&a[e]));
+          fb = __half22float2(*reinterpret_cast<const __half2*>(&b[e]));
+          fc = __half22float2(*reinterpret_cast<const __half2*>(&cc[e]));
+          fs = __half22float2(*reinterpret_cast<const __half2*>(&ss[e]));
+        }
+        // same expression as the standalone rope kernel (k_rope.cu)
+        const float r0x = fa.x * fc.x - fb.x * fs.x, r0y = fa.y * fc.y - fb.y * fs.y;
+        const float r1x = fa.x * fs.x + fb.x * fc.x, r1y = fa.y * fs.y + fb.y * fc.y;
+        o0[e] = BF16 ? sm100::pack_bf16(r0x, r0y) : sm100::pack_f16(r0x, r0y);
+        o1[e] = BF16 ? sm100::pack_bf16(r1x, r1y) : sm100::pack_f16(r1x, r1y);
+      }
+      *p0[k] = make_uint4(o0[0], o0[1], o0[2], o0[3]);
+      *p1[k] = make_uint4(o1[0], o1[1], o1[2], o1[3]);
+    }
+  }
+}
+
+template <int D, bool ROPE = false>
 struct Layout {
   static constexpr int DCH = D / 64;               // 128B chunks along D
   static constexpr int Q_BYTES = BM * D * 2;       // one query tile
@@ -96,12 +173,14 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x for a pair on the FMA pipe: x clamped to [-127, .], x = i + f with
+// 2^x for a pair on the FMA pipe: x clamped to [-125, .] (2^i with i >= -125
+// keeps the exponent add from wrapping into the sign bit; masked keys, -inf,
+// give ~2^-125 instead of 0, below the 16-bit P resolution), x = i + f with
 // i = rint(x) (1.5*2^23 trick), f in [-0.5, 0.5]; 2^f by a cubic (rel. err
 // 7.5e-5, below half an fp16 / bf16 ulp); 2^i added into the exponent.
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
   const float2 magic = make_float2(12582912.0f, 12582912.0f);
   const float2 t = __fadd2_rn(x, magic);
   const float2 r = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
@@ -119,16 +198,16 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return BF16 ? sm100::pack_bf16(a, b) : sm100::pack_f16(a, b);
 }
 
-template <int D, bool BF16>
+template <int D, bool BF16, bool ROPE>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_kernel(const __grid_constant__ AttnMaps maps, const AttnParams p) {
   using namespace sm100;
-  using L = Layout<D>;
+  using L = Layout<D, ROPE>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t q_full, q_empty, kv_full[L::NS], kv_empty[L::NS], s_full[2],
-      p_full[2][2], o_full[2], o_empty[2];
+      p_full[2][2], o_full[2], o_empty[2], q_rot;
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -148,6 +227,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&o_full[g], 1);
       mbar_init(&o_empty[g], 4);
     }
+    mbar_init(&q_rot, 2);                       // rope warps 2-3
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -231,7 +311,7 @@ __global__ void __launch_bounds__(384, 1)
         }
       };
       for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
-        mbar_wait(&q_full, it & 1);
+        mbar_wait(ROPE ? &q_rot : &q_full, it & 1);
         tc_fence_after();
         wait_kv(c);
         issue_s(0, c);
@@ -288,6 +368,25 @@ __global__ void __launch_bounds__(384, 1)
         }
         c += 2 * n_kv;
       }
+    }
+  } else if (ROPE && (warp == 2 || warp == 3)) {
+    // rotary embedding of the two Q tiles of every item, in shared memory
+    // between the TMA load and the first S MMA.  (K is rotated once per
+    // (b, h) by a pre-pass: rotating every K tile here measured 20.2 ms vs
+    // 7.2 ms, because the 16 query blocks that share a K tile each redo it
+    // and the table reads double the L2 stream.)
+    const int t = (warp - 2) * 32 + lane;
+    int it = 0;
+    for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+      const int qt = item % p.n_qt;
+      mbar_wait(&q_full, it & 1);
+#pragma unroll 1
+      for (int g = 0; g < 2; ++g)
+        rope_tile<D, BF16>(smem + L::OFF_Q + g * L::Q_BYTES, BM * 128, BM,
+                           qt * 2 * BM + g * BM, p.Sq, p.sin_q, p.sq_rs, p.cos_q, p.cq_rs, t, 64);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&q_rot);
     }
   }
   } else {
@@ -436,10 +535,10 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-template <int D, bool BF16>
+template <int D, bool BF16, bool ROPE>
 int launch_attn(const AttnMaps& maps, const AttnParams& p, cudaStream_t s) {
-  using L = Layout<D>;
-  auto k = attn_fwd_kernel<D, BF16>;
+  using L = Layout<D, ROPE>;
+  auto k = attn_fwd_kernel<D, BF16, ROPE>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
@@ -483,7 +582,7 @@ bool map4(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int64_t D, i
 
 }  // namespace
 
-int attn_sm100(const AttnDesc& a, int dtype, cudaStream_t s) {
+int attn_sm100(const AttnDesc& a, int dtype, cudaStream_t s, const RopeTables* rope, bool dry_run) {
   if (a.D != 64 && a.D != 128) return NTB_ERR_UNSUPPORTED;
   if (a.Sk < 1 || a.Sq < 1 || a.B >= 65536 || a.H >= 65536 || a.Sq >= (1 << 30) ||
       a.Sk >= (1 << 30))
@@ -522,8 +621,30 @@ int attn_sm100(const AttnDesc& a, int dtype, cudaStream_t s) {
   p.scale_log2 = a.scale * kLog2e;
   p.o = a.o;
   for (int i = 0; i < 4; ++i) p.os[i] = a.os[i];
-  if (a.D == 128) return bf16 ? launch_attn<128, true>(maps, p, s) : launch_attn<128, false>(maps, p, s);
-  return bf16 ? launch_attn<64, true>(maps, p, s) : launch_attn<64, false>(maps, p, s);
+  p.sin_q = p.cos_q = nullptr;
+  p.sq_rs = p.cq_rs = 0;
+  if (rope) {
+    // tables (S, D/2): 16-byte aligned rows of contiguous columns, covering
+    // every query / key position
+    const void* tp[2] = {rope->sin_q, rope->cos_q};
+    const int64_t* tr[2] = {rope->sq, rope->cq};
+    for (int i = 0; i < 2; ++i) {
+      const int64_t rows_needed = a.Sq;
+      if (!aligned16(tp[i]) || tr[i][3] != 1 || tr[i][1] != a.D / 2 ||
+          (tr[i][2] * 2) % 16 || (tr[i][0] < rows_needed))
+        return NTB_ERR_UNSUPPORTED;
+    }
+    p.sin_q = rope->sin_q; p.sq_rs = rope->sq[2];
+    p.cos_q = rope->cos_q; p.cq_rs = rope->cq[2];
+    if (dry_run) return NTB_OK;
+    if (a.D == 128)
+      return bf16 ? launch_attn<128, true, true>(maps, p, s) : launch_attn<128, false, true>(maps, p, s);
+    return bf16 ? launch_attn<64, true, true>(maps, p, s) : launch_attn<64, false, true>(maps, p, s);
+  }
+  if (dry_run) return NTB_OK;
+  if (a.D == 128)
+    return bf16 ? launch_attn<128, true, false>(maps, p, s) : launch_attn<128, false, false>(maps, p, s);
+  return bf16 ? launch_attn<64, true, false>(maps, p, s) : launch_attn<64, false, false>(maps, p, s);
 }
 
 }  // namespace ntb

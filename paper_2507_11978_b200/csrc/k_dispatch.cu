@@ -98,6 +98,90 @@ int launch_conv2d(const LaunchArgs& A) {
   return conv_generic(c, A.dtype, A.stream);
 }
 
+static int fill_attn(const LaunchArgs& A, int qi, int ki, int vi, int oi, AttnDesc& a) {
+  for (int i : {qi, ki, vi, oi})
+    if (A.ranks[i] != 4) return fail(NTB_ERR_ARG, "sdpa: rank-4 (B, H, S, D) tensors");
+  const int64_t* S = A.sizes;
+  const int64_t* T = A.strides;
+  const int64_t q0 = A.base[qi], k0 = A.base[ki], v0 = A.base[vi], o0 = A.base[oi];
+  a.q = A.ptrs[qi];
+  a.k = A.ptrs[ki];
+  a.v = A.ptrs[vi];
+  a.o = A.ptrs[oi];
+  a.B = S[q0];
+  a.H = S[q0 + 1];
+  a.Sq = S[q0 + 2];
+  a.D = S[q0 + 3];
+  a.Sk = S[k0 + 2];
+  for (int d = 0; d < 4; ++d) {
+    a.qs[d] = T[q0 + d];
+    a.ks[d] = T[k0 + d];
+    a.vs[d] = T[v0 + d];
+    a.os[d] = T[o0 + d];
+  }
+  if (S[v0 + 2] != a.Sk || S[k0 + 3] != a.D || S[v0 + 3] != a.D || S[o0 + 2] != a.Sq ||
+      S[o0 + 3] != a.D)
+    return fail(NTB_ERR_UNSUPPORTED, "sdpa: inconsistent K/V/O extents");
+  a.scale = 1.0f / sqrtf((float)a.D);
+  return NTB_OK;
+}
+
+// sdpa(rope(q), rope(k), v): params q, k, v, sin_q, cos_q, sin_k, cos_k, o
+// (catalog.spec_sdpa_rope).  Q is rotated inside the attention kernel (in
+// shared memory between its TMA load and the first MMA, once per query
+// tile); K is rotated once per (b, h) by a vectorised pre-pass into library
+// workspace (same layout as k), because in-kernel K rotation is redone by
+// every query block that shares the K tile.
+int launch_sdpa_rope(const LaunchArgs& A) {
+  if (A.n_ptrs != 8) return fail(NTB_ERR_ARG, "sdpa_rope: expects q, k, v, sin_q, cos_q, sin_k, cos_k, o");
+  AttnDesc a = {};
+  int rc = fill_attn(A, 0, 1, 2, 7, a);
+  if (rc) return rc;
+  for (int i = 3; i < 7; ++i)
+    if (A.ranks[i] != 2) return fail(NTB_ERR_ARG, "sdpa_rope: rotary tables are (S, D/2)");
+  if (A.dtype != NTB_F16 && A.dtype != NTB_BF16)
+    return fail(NTB_ERR_UNSUPPORTED, "sdpa_rope: fp16 / bf16 only");
+  const char* layout_msg =
+      "sdpa_rope: the fused path needs D in {64, 128}, q/k/v 16-byte aligned with unit inner "
+      "stride, k contiguous as (B, S, H, D) or (B, H, S, D), and contiguous (S, D/2) tables "
+      "covering every position; run rope_launch + sdpa_launch for other layouts";
+  // K pre-pass
+  const int64_t B = a.B, H = a.H, S = a.Sk, D = a.D;
+  const int64_t* ks = a.ks;
+  int64_t pos_div;
+  if (ks[3] == 1 && ks[1] == D && ks[2] == H * D && (B == 1 || ks[0] == S * H * D)) pos_div = H;
+  else if (ks[3] == 1 && ks[2] == D && ks[1] == S * D && (B == 1 || ks[0] == H * S * D)) pos_div = 1;
+  else return fail(NTB_ERR_UNSUPPORTED, layout_msg);
+  const int64_t sb = A.base[5], cb = A.base[6];
+  if (A.sizes[sb] < S || A.sizes[cb] < S || A.sizes[sb + 1] != D / 2 || A.sizes[cb + 1] != D / 2 ||
+      A.strides[sb] != D / 2 || A.strides[cb] != D / 2 || A.strides[sb + 1] != 1 ||
+      A.strides[cb + 1] != 1 || !aligned16(A.ptrs[5]) || !aligned16(A.ptrs[6]) ||
+      !aligned16(a.k) || (D != 64 && D != 128))
+    return fail(NTB_ERR_UNSUPPORTED, layout_msg);
+  void* krot = workspace((size_t)(B * H * S * D) * 2, A.stream);
+  if (!krot) return fail(NTB_ERR_CUDA, "sdpa_rope: workspace allocation failed");
+  RopeTables rt;
+  rt.sin_q = A.ptrs[3];
+  rt.cos_q = A.ptrs[4];
+  for (int d = 0; d < 2; ++d) {
+    rt.sq[d] = A.sizes[A.base[3] + d];
+    rt.cq[d] = A.sizes[A.base[4] + d];
+    rt.sq[2 + d] = A.strides[A.base[3] + d];
+    rt.cq[2 + d] = A.strides[A.base[4] + d];
+  }
+  // the attention kernel validates q / v / o and the query tables without
+  // launching; only then run the K pre-pass
+  AttnDesc ak = a;
+  ak.k = krot;
+  rc = attn_sm100(ak, A.dtype, A.stream, &rt, /*dry_run=*/true);
+  if (rc == NTB_ERR_UNSUPPORTED) return fail(NTB_ERR_UNSUPPORTED, layout_msg);
+  if (rc) return rc;
+  rc = rope_rows_vec(a.k, A.ptrs[5], A.ptrs[6], krot, B * H * S, S, pos_div, (int)(D / 2),
+                     A.dtype, A.stream);
+  if (rc) return rc;
+  return attn_sm100(ak, A.dtype, A.stream, &rt);
+}
+
 int launch_sdpa(const LaunchArgs& A) {
   if (A.n_ptrs != 4) return fail(NTB_ERR_ARG, "sdpa: expects q, k, v, o");
   for (int i = 0; i < 4; ++i)

@@ -11,6 +11,7 @@
 // the same packs of the second half; tables (S x HALF) stay L2-resident.
 // HBM roofline: 2 x B*S*H*D*sizeof(T) (+ the tables once).
 #include "common.cuh"
+#include "k_sm100.cuh"
 
 namespace ntb {
 
@@ -132,6 +133,25 @@ static int run_rope(const LaunchArgs& A) {
         half);
   }
   return check_launch("rope", NTB_PATH_ROPE_GENERIC);
+}
+
+int rope_rows_vec(const void* x, const void* sn, const void* cs, void* out, int64_t rows,
+                  int64_t S, int64_t pos_div, int half, int dtype, cudaStream_t s) {
+  const int sms = sm_count();
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    constexpr int N = Pack<T>::N;
+    int64_t items = rows * (half / N);
+    int64_t blocks = cdiv64(items, 256);
+    if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    if (blocks < 1) blocks = 1;
+    launch_pdl(rope_vec_kernel<T>, dim3((unsigned)blocks), dim3(256), 0, s, (const T*)x,
+               (const T*)sn, (const T*)cs, (T*)out, rows, S, pos_div, half);
+    return check_launch("rope (sdpa_rope K pre-pass)", NTB_PATH_ROPE_VEC);
+  };
+  if (dtype == NTB_F16) return go(__half());
+  if (dtype == NTB_BF16) return go(__nv_bfloat16());
+  return NTB_ERR_UNSUPPORTED;
 }
 
 int launch_rope(const LaunchArgs& A) {

@@ -9,6 +9,19 @@ namespace ntb {
 
 int gemm_sm100(const GemmDesc& g, int dtype, cudaStream_t s);
 int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s);
-int attn_sm100(const AttnDesc& a, int dtype, cudaStream_t s);
+// Query-side rotary tables for sdpa_rope: {rows, cols, row_stride,
+// col_stride} in elements.  The kernel rotates Q tiles in shared memory; K
+// arrives already rotated (launch_sdpa_rope's pre-pass).
+struct RopeTables {
+  const void *sin_q, *cos_q;
+  int64_t sq[4], cq[4];
+};
+// Half-split rotary embedding of `rows` contiguous rows of 2*half elements
+// (position of row r = (r / pos_div) % S; tables (S, half), row stride half).
+int rope_rows_vec(const void* x, const void* sn, const void* cs, void* out, int64_t rows,
+                  int64_t S, int64_t pos_div, int half, int dtype, cudaStream_t s);
+// dry_run: validate the layout contract (and build the tensor maps) without launching.
+int attn_sm100(const AttnDesc& a, int dtype, cudaStream_t s, const RopeTables* rope = nullptr,
+               bool dry_run = false);
 
 }  // namespace ntb

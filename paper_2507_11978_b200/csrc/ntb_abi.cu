@@ -296,6 +296,7 @@ int ntb_launch(int kernel, int dtype, void* const* ptrs, int n_ptrs, const doubl
     case NTB_K_ADDMM: return launch_gemm(a);
     case NTB_K_CONV2D: return launch_conv2d(a);
     case NTB_K_SDPA: return launch_sdpa(a);
+    case NTB_K_SDPA_ROPE: return launch_sdpa_rope(a);
     default: return fail(NTB_ERR_UNSUPPORTED, "unknown kernel family");
   }
 }

@@ -41,6 +41,7 @@ int launch_rope(const LaunchArgs& a);
 int launch_gemm(const LaunchArgs& a);          // mm, bmm, addmm
 int launch_conv2d(const LaunchArgs& a);
 int launch_sdpa(const LaunchArgs& a);
+int launch_sdpa_rope(const LaunchArgs& a);
 
 // Device workspace (grown on demand, stream-ordered use only).
 void* workspace(size_t bytes, cudaStream_t s);

@@ -118,3 +118,23 @@ def test_non_catalog_spec_is_rejected():
     with pytest.raises(backend.UnsupportedSpecError):
         backend.launch(typecheck(spec), {"input": _Fake((8,)), "output": _Fake((8,))},
                        {"BLOCK_SIZE": 4})
+
+
+def test_sdpa_rope_table_rows_checked_before_launch():
+    """The query-side tables must block like the query rows (grid check,
+    evaluated by the native map VM before any device work)."""
+    ck = C.checked("sdpa_rope")
+    b, h, s, d = 2, 3, 300, 64
+    args = {"q": _Fake((b, h, s, d)), "k": _Fake((b, h, s, d)), "v": _Fake((b, h, s, d)),
+            "sin_q": _Fake((100, d // 2)), "cos_q": _Fake((s, d // 2)),
+            "sin_k": _Fake((s, d // 2)), "cos_k": _Fake((s, d // 2)),
+            "o": _Fake((b, h, s, d))}
+    with pytest.raises(backend.LaunchError, match="launch-time check failed"):
+        backend.launch(ck, args, {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128})
+
+
+def test_sdpa_rope_is_its_own_family():
+    assert backend._family_of(C.checked("sdpa_rope")) == "sdpa_rope"
+    assert _lib.KERNEL_IDS["sdpa_rope"] == 11
+    hdr = Path(__file__).resolve().parent.parent / "include" / "ntb200.h"
+    assert "NTB_K_SDPA_ROPE = 11" in hdr.read_text()

@@ -114,4 +114,14 @@ def test_builder_defined_specs_typecheck():
     assert [S.text(s) for s in sd.index_maps["k"].nest_sizes] == ["cdiv(k_size_2, BLOCK_SIZE_N)"]
     rp = C.checked("rope")
     assert [S.text(s) for s in rp.grid.sizes] == ["input_size_1", "input_size_0 * input_size_2"]
+    fr = C.checked("sdpa_rope")
+    assert [S.text(s) for s in fr.grid.sizes] == ["q_size_0 * q_size_1",
+                                                  "cdiv(q_size_2, BLOCK_SIZE_M)"]
+    # query-side tables follow the program (outer) level, key-side tables
+    # the K/V nest
+    assert fr.index_maps["sin_q"].nest_sizes == ()
+    assert [S.text(s) for s in fr.index_maps["cos_k"].nest_sizes] == \
+        ["cdiv(cos_k_size_0, BLOCK_SIZE_N)"]
+    checks = [(S.text(a), S.text(b)) for a, b in fr.grid.checks]
+    assert ("cdiv(q_size_2, BLOCK_SIZE_M)", "cdiv(sin_q_size_0, BLOCK_SIZE_M)") in checks
     assert [S.text(s) for s in rp.index_maps["input"].nest_sizes] == ["cdiv(input_size_3, HALF_D)"]

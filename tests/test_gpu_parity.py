@@ -109,7 +109,8 @@ class _Paths:
 
 def _close(got, ref, rtol=1e-2, atol=1e-2):
     got = got.float().cpu().numpy().astype(np.float64)
-    bad = np.abs(got - ref) > atol + rtol * np.abs(ref)
+    assert np.isfinite(got).all(), f"{(~np.isfinite(got)).sum()} non-finite outputs"
+    bad = ~(np.abs(got - ref) <= atol + rtol * np.abs(ref))
     assert not bad.any(), f"{bad.sum()} of {bad.size} outside tol; max err " \
                           f"{np.max(np.abs(got - ref)):.3e}"
 
@@ -286,6 +287,47 @@ def test_sdpa_peaky_scores_rescale(d):
                {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128}, torch.float16,
                out=torch.zeros((b, h, s, d), device=DEV, dtype=torch.float16))
     _close(got, oracle.sdpa(q, k, v), rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("dtype", DTS)
+@pytest.mark.parametrize("bshd", [(1, 256, 2, 64), (2, 300, 3, 128), (2, 1024, 4, 128),
+                                  (3, 700, 40, 64), (1, 520, 64, 128)])
+def test_sdpa_rope_fused(dtype, bshd):
+    """sdpa(rope(q), rope(k), v) in ONE kernel (rotary embedding applied in
+    shared memory between the TMA loads and the MMAs) against (1) the oracle
+    fed the rotated Q/K rounded to the device dtype, as the device rounds them
+    before its 16-bit products, and (2) the unfused rope_launch x2 +
+    sdpa_launch pipeline.  Q/K/V are (B, S, H, D) storage viewed as
+    (B, H, S, D), the paper's layout."""
+    b, s, h, d = bshd
+    rng = np.random.default_rng(s + d)
+    base = [_r16(rng.uniform(-1, 1, (b, s, h, d)).astype(np.float32), dtype) for _ in range(3)]
+    ang = rng.uniform(-3, 3, (s, d // 2))
+    sn = _r16(np.sin(ang).astype(np.float32), dtype)
+    cs = _r16(np.cos(ang).astype(np.float32), dtype)
+    tq, tk, tv = (_t(x, dtype) for x in base)
+    tsn, tcs = _t(sn, dtype), _t(cs, dtype)
+    q, k, v = (t.transpose(1, 2) for t in (tq, tk, tv))
+    o = torch.zeros((b, h, s, d), device=DEV, dtype=dtype)
+    with _Paths() as pc:
+        backend.sdpa_rope_launch(q, k, v, tsn, tcs, tsn, tcs, o, 128, 128)
+        torch.cuda.synchronize()
+    assert pc.delta["attn_tc"] == 1
+
+    def rot(x):
+        r = oracle.rope_bhsd(np.swapaxes(x, 1, 2), sn, cs)
+        return torch.from_numpy(r.astype(np.float32)).to(dtype).float().numpy()
+
+    ref = oracle.sdpa(rot(base[0]), rot(base[1]), np.swapaxes(base[2], 1, 2))
+    _close(o, ref, rtol=1e-2, atol=1e-2)
+    # unfused pipeline on the same inputs
+    qr, kr = torch.empty_like(tq), torch.empty_like(tk)
+    backend.rope_launch(tq, tsn, tcs, qr, d // 2)
+    backend.rope_launch(tk, tsn, tcs, kr, d // 2)
+    o2 = torch.zeros_like(o)
+    backend.sdpa_launch(qr.transpose(1, 2), kr.transpose(1, 2), v, o2, 128, 128)
+    torch.cuda.synchronize()
+    assert (o.float() - o2.float()).abs().max().item() <= 2e-3
 
 
 def test_sdpa_strided_views():
