@@ -82,7 +82,8 @@ enum {
   NTB_PATH_ATTN_TC = 11, NTB_PATH_ATTN_GENERIC = 12,
   NTB_PATH_REPACK = 13,
   NTB_PATH_ROW_STREAM = 14,
-  NTB_NUM_PATHS = 15
+  NTB_PATH_JIT = 15,
+  NTB_NUM_PATHS = 16
 };
 int64_t ntb_path_count(int path);
 
@@ -149,6 +150,18 @@ int ntb_launch(int kernel, int dtype,
                const int* ranks,
                const int64_t* meta, int n_meta,
                void* stream);
+
+/* ---- generic path --------------------------------------
+ * Specs that match no native family are printed as CUDA C++ by the host front
+ * end (codegen.py; replaces the reference's Triton emitter, emit.py:72-314) and
+ * compiled here with NVRTC for sm_100a.  Handles are cached per (source,
+ * device).  Errors: NTB_ERR_UNSUPPORTED (no NVRTC / compile error, text in
+ * ntb_last_error), NTB_ERR_CUDA, NTB_ERR_ARG. */
+int ntb_jit_compile(const char* source, const char* kernel_name, int64_t* handle_out);
+/* grid3 / block3: launch dims; args: cuLaunchKernel-style pointers to each
+ * kernel argument; stream: cudaStream_t or NULL. */
+int ntb_jit_launch(int64_t handle, const int64_t* grid3, const int64_t* block3, void** args,
+                   void* stream);
 
 /* Device scratch used by ntb_launch for strided-operand repacking; freed by
  * ntb_release_workspace (optional; the library frees it at unload).       */

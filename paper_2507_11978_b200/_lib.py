@@ -25,7 +25,7 @@ KERNEL_IDS = {"add": 1, "silu": 2, "softmax": 3, "rms_norm": 4, "mm": 5, "bmm": 
 EXPORTS = ("ntb_abi_version", "ntb_last_error", "ntb_launch_count", "ntb_path_count",
            "ntb_expr_eval",
            "ntb_grid_eval", "ntb_map_enumerate", "ntb_map_probe", "ntb_launch",
-           "ntb_release_workspace")
+           "ntb_release_workspace", "ntb_jit_compile", "ntb_jit_launch")
 
 _lib = None
 
@@ -63,8 +63,11 @@ def lib():
                              ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
                              _i64p, _i64p, ctypes.POINTER(ctypes.c_int), _i64p, ctypes.c_int,
                              ctypes.c_void_p]
+    L.ntb_jit_compile.argtypes = [ctypes.c_char_p, ctypes.c_char_p, _i64p]
+    L.ntb_jit_launch.argtypes = [ctypes.c_int64, _i64p, _i64p, ctypes.POINTER(ctypes.c_void_p),
+                                 ctypes.c_void_p]
     for name in ("ntb_expr_eval", "ntb_grid_eval", "ntb_map_enumerate", "ntb_map_probe",
-                 "ntb_launch", "ntb_release_workspace"):
+                 "ntb_launch", "ntb_release_workspace", "ntb_jit_compile", "ntb_jit_launch"):
         getattr(L, name).restype = ctypes.c_int
     if L.ntb_abi_version() != 1:
         raise NativeLibraryError("libntb200 ABI version mismatch")
@@ -115,7 +118,7 @@ def map_enumerate(blob: np.ndarray, param: int, slots: np.ndarray):
 
 
 PATHS = ("probe", "ew_vec", "ew_generic", "row_vec", "row_generic", "rope_vec", "rope_generic",
-         "gemm_tc", "gemm_generic", "conv_tc", "conv_generic", "attn_tc", "attn_generic", "repack", "row_stream")
+         "gemm_tc", "gemm_generic", "conv_tc", "conv_generic", "attn_tc", "attn_generic", "repack", "row_stream", "jit")
 
 
 def path_counts() -> dict:
@@ -125,3 +128,17 @@ def path_counts() -> dict:
 
 def loaded_path() -> str:
     return os.fspath(LIB_PATH)
+
+
+def jit_compile(source: str, kernel_name: str) -> int:
+    """NVRTC-compile generated CUDA C++ for sm_100a (cached per source)."""
+    h = np.zeros(1, dtype=np.int64)
+    rc = lib().ntb_jit_compile(source.encode(), kernel_name.encode(), i64(h))
+    return rc, int(h[0])
+
+
+def jit_launch(handle: int, grid3, block3, arg_ptrs, stream) -> int:
+    g = np.asarray(grid3, dtype=np.int64)
+    b = np.asarray(block3, dtype=np.int64)
+    arr = (ctypes.c_void_p * len(arg_ptrs))(*arg_ptrs)
+    return lib().ntb_jit_launch(handle, i64(g), i64(b), arr, ctypes.c_void_p(stream))

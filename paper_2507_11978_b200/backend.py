@@ -219,13 +219,22 @@ def _family_of(checked) -> str:
         "arrangement and application it has a native kernel for")
 
 
-def _resolve(checked) -> tuple:
+def _resolve(checked, allow_generic: bool = False) -> tuple:
+    """(family, map program).  family is None for a spec that matches no
+    native kernel family when ``allow_generic`` (the generated-code path)."""
     key = id(checked)
     with _cache_lock:
         hit = _cache.get(key)
         if hit is not None and hit[0] is checked:
+            if hit[1] is None and not allow_generic:
+                _family_of(checked)   # raises UnsupportedSpecError
             return hit[1], hit[2]
-    family = _family_of(checked)
+    try:
+        family = _family_of(checked)
+    except UnsupportedSpecError:
+        if not allow_generic:
+            raise
+        family = None
     prog = build_program(checked)
     with _cache_lock:
         _cache[key] = (checked, family, prog)
@@ -272,7 +281,7 @@ def _check_failure(prog: MapProgram, binding: dict) -> str:
 
 def evaluate_grid(checked, binding: dict) -> tuple:
     """Checks + grid through the native map VM (ntb_grid_eval)."""
-    _, prog = _resolve(checked)
+    _, prog = _resolve(checked, allow_generic=True)
     rc, grid = _lib.grid_eval(prog.blob, prog.slots(binding))
     if rc == _lib.NTB_ERR_CHECK:
         raise LaunchError(_check_failure(prog, binding))
@@ -323,6 +332,8 @@ def launch(checked, args: Mapping, meta: Mapping, *, stream=None) -> LaunchResul
         if len(_plans) > _PLAN_CAP:
             _plans.clear()
         _plans[key] = plan
+    if plan[1] == "jit":
+        return _launch_generated(plan, args, stream)
     _, names, kid, dt, n, sizes, strides, ranks, metas, sc, n_sc, result, dev = plan
     ptrs = (ctypes.c_void_p * n)(*[args[nm].data_ptr() for nm in names])
     if stream is None:
@@ -339,12 +350,69 @@ def launch(checked, args: Mapping, meta: Mapping, *, stream=None) -> LaunchResul
     return result
 
 
+def _launch_generated(plan, args: Mapping, stream):
+    import torch
+
+    _, _, handle, names, scalars, slots, block, grid_total, result, dev = plan
+    store = [ctypes.c_void_p(args[nm].data_ptr()) for nm in names]
+    store += [ctypes.c_float(v) for v in scalars]
+    ptrs = [ctypes.addressof(c) for c in store] + [slots.ctypes.data]
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    with torch.cuda.device(dev):
+        rc = _lib.jit_launch(handle, (grid_total, 1, 1), (block, 1, 1), ptrs, stream)
+    if rc:
+        raise BackendError(_lib.last_error())
+    return result
+
+
+def _make_generated_plan(checked, binding, prog, grid, args):
+    """Generic path: CUDA C++ printed from the spec by
+    codegen.py, NVRTC-compiled for sm_100a through the C ABI."""
+    import torch
+
+    from . import codegen
+
+    spec = checked.spec
+    tensors = [p for p in spec.params if p.rank >= 1]
+    ts = [args[p.name] for p in tensors]
+    dt = _dtype_code(ts[0]) if isinstance(ts[0], torch.Tensor) else 0
+    try:
+        gen = codegen.generate(checked, binding, dt)
+    except codegen.CodegenError as e:
+        raise UnsupportedSpecError(
+            f"spec {spec.name!r} matches no sm_100a kernel family and the generic path does not "
+            f"cover it: {e}") from None
+    for p, t in zip(tensors, ts):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise LaunchError(
+                f"argument {p.name!r} must be a CUDA tensor (the B200 backend has no CPU path)")
+    for p, t in zip(tensors, ts):
+        if _dtype_code(t) != dt or t.device != ts[0].device:
+            raise LaunchError(f"argument {p.name!r} must match {ts[0].dtype} on {ts[0].device}")
+    with torch.cuda.device(ts[0].device):
+        rc, handle = _lib.jit_compile(gen.source, gen.name)
+    if rc == _lib.NTB_ERR_UNSUPPORTED:
+        raise UnsupportedSpecError(_lib.last_error())
+    if rc:
+        raise BackendError(_lib.last_error())
+    scalars = []
+    for p in spec.params:
+        if p.rank == 0:
+            v = args[p.name]
+            scalars.append(float(v.item() if hasattr(v, "item") else v))
+    slots = np.array([binding[n] for n in gen.slot_names] or [0], dtype=np.int64)
+    total = int(np.prod(grid))
+    return ("jit", handle, gen.tensor_params, scalars, slots, gen.block, total,
+            LaunchResult(grid=tuple(grid), total=total), ts[0].device)
+
+
 def _make_plan(checked, args: Mapping, meta: Mapping):
     import torch
 
     spec = checked.spec
     binding = _binding(spec, args, meta)
-    family, prog = _resolve(checked)
+    family, prog = _resolve(checked, allow_generic=True)
     rc, grid = _lib.grid_eval(prog.blob, prog.slots(binding))
     if rc == _lib.NTB_ERR_CHECK:
         raise LaunchError(_check_failure(prog, binding))
@@ -353,6 +421,8 @@ def _make_plan(checked, args: Mapping, meta: Mapping):
     if rc:
         raise BackendError(_lib.last_error())
     total = int(np.prod(grid))
+    if family is None:
+        return _make_generated_plan(checked, binding, prog, grid, args)
 
     tensors = [p for p in spec.params if p.rank >= 1]
     ts = [args[p.name] for p in tensors]

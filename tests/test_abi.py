@@ -108,16 +108,29 @@ def test_rms_norm_padded_width_check():
         backend.launch(C.checked("rms_norm"), args, {"COLS_PADDED": 16})
 
 
-def test_non_catalog_spec_is_rejected():
+def test_non_catalog_spec_takes_the_generic_path_and_needs_cuda_tensors():
+    """A spec outside the native families is code-generated (codegen.py); the
+    generated path, like every other, refuses host tensors (no CPU path)."""
     from paper_2507_11978_b200.spec import KernelSpec, ParamSpec, Store, Load, typecheck, ArrangeOp
-    spec = KernelSpec("add", (ParamSpec("input", 1, "f32", "in"), ParamSpec("output", 1, "f32", "out")),
+    spec = KernelSpec("copy", (ParamSpec("input", 1, "f32", "in"), ParamSpec("output", 1, "f32", "out")),
                       ("BLOCK_SIZE",),
                       {"input": (ArrangeOp("tile", shape=(S.var("BLOCK_SIZE"),)),),
                        "output": (ArrangeOp("tile", shape=(S.var("BLOCK_SIZE"),)),)},
                       (Store("output", Load("input")),))
-    with pytest.raises(backend.UnsupportedSpecError):
+    with pytest.raises(backend.LaunchError, match="CUDA tensor"):
         backend.launch(typecheck(spec), {"input": _Fake((8,)), "output": _Fake((8,))},
                        {"BLOCK_SIZE": 4})
+
+
+def test_spec_outside_generic_subset_is_unsupported():
+    from paper_2507_11978_b200.spec import (ArrangeOp, BinOp, Dot, KernelSpec, Load, ParamSpec,
+                                            Store, typecheck)
+    t = (ArrangeOp("tile", shape=(S.var("B"), S.var("B"))),)
+    spec = KernelSpec("sq", (ParamSpec("a", 2, "f16", "in"), ParamSpec("c", 2, "f16", "out")),
+                      ("B",), {"a": t, "c": t},
+                      (Store("c", BinOp("+", Dot(Load("a"), Load("a")), Load("a"))),))
+    with pytest.raises(backend.UnsupportedSpecError, match="generic path"):
+        backend.launch(typecheck(spec), {"a": _Fake((8, 8)), "c": _Fake((8, 8))}, {"B": 4})
 
 
 def test_sdpa_rope_table_rows_checked_before_launch():

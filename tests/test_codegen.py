@@ -1,0 +1,148 @@
+"""Generic path: specs that match no native kernel
+family are printed as CUDA C++ (codegen.py) and NVRTC-compiled for sm_100a by
+the C ABI (ntb_jit_compile).  CPU tests: the generated source compiles for
+sm_100a with NVRTC; GPU tests: results against numpy."""
+
+import numpy as np
+import pytest
+
+from paper_2507_11978_b200 import backend, codegen
+from paper_2507_11978_b200.make import Symbol, Tensor, language as ntl, make
+
+BLOCK = Symbol("BLOCK", constexpr=True)
+
+
+def fma_kernel():
+    def arrangement(x, y, z, out, BLOCK=BLOCK):
+        return x.tile((BLOCK,)), y.tile((BLOCK,)), z.tile((BLOCK,)), out.tile((BLOCK,))
+
+    def application(x, y, z, out):
+        out = x * y + z  # noqa: F841
+
+    return make(arrangement, application, (Tensor(1), Tensor(1), Tensor(1), Tensor(1)))
+
+
+def gelu_kernel():
+    def arrangement(x, out, BLOCK=BLOCK):
+        return x.tile((BLOCK,)), out.tile((BLOCK,))
+
+    def application(x, out):
+        out = x * ntl.sigmoid(1.702 * x)  # noqa: F841
+
+    return make(arrangement, application, (Tensor(1), Tensor(1)))
+
+
+def temp_softmax_kernel():
+    def arrangement(x, out, BLOCK=BLOCK):
+        return x.tile((1, BLOCK)), out.tile((1, BLOCK))
+
+    def application(x, out):
+        z = x * 0.5
+        e = ntl.exp(z - ntl.max(z))
+        out = e / ntl.sum(e)  # noqa: F841
+
+    return make(arrangement, application, (Tensor(2, other=float("-inf")), Tensor(2)))
+
+
+def l2norm_kernel():
+    def arrangement(x, out, BLOCK=BLOCK):
+        return x.tile((1, BLOCK)), out.tile((1, BLOCK))
+
+    def application(x, out):
+        out = x / ntl.sqrt(ntl.sum(x * x) + 1e-6)  # noqa: F841
+
+    return make(arrangement, application, (Tensor(2), Tensor(2)))
+
+
+def _binding(k, shapes, meta):
+    b = dict(meta)
+    for p, shp in zip(k.checked.spec.params, shapes):
+        st, acc = [], 1
+        for s in reversed(shp):
+            st.append(acc)
+            acc *= s
+        for i, (s, t) in enumerate(zip(shp, reversed(st))):
+            b[f"{p.name}_size_{i}"] = s
+            b[f"{p.name}_stride_{i}"] = t
+    return b
+
+
+CASES = [
+    (fma_kernel, [(5000,)] * 4, {"BLOCK": 1024}),
+    (gelu_kernel, [(777,)] * 2, {"BLOCK": 256}),
+    (temp_softmax_kernel, [(33, 1000)] * 2, {"BLOCK": 1024}),
+    (l2norm_kernel, [(7, 4096)] * 2, {"BLOCK": 4096}),
+]
+
+
+@pytest.mark.parametrize("build,shapes,meta", CASES)
+def test_generated_source_compiles_for_sm100a(build, shapes, meta):
+    nvrtc = pytest.importorskip("cuda.bindings.nvrtc")
+    k = build()
+    with pytest.raises(backend.UnsupportedSpecError):
+        backend._family_of(k.checked)          # not a native family
+    for dt in (0, 1, 2):
+        g = codegen.generate(k.checked, _binding(k, shapes, meta), dt)
+        err, prog = nvrtc.nvrtcCreateProgram(g.source.encode(), b"gen.cu", 0, [], [])
+        assert err == nvrtc.nvrtcResult.NVRTC_SUCCESS
+        opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-default-device",
+                b"--include-path=/usr/local/cuda/include"]
+        err, = nvrtc.nvrtcCompileProgram(prog, len(opts), opts)
+        if err != nvrtc.nvrtcResult.NVRTC_SUCCESS:
+            _, n = nvrtc.nvrtcGetProgramLogSize(prog)
+            log = b" " * n
+            nvrtc.nvrtcGetProgramLog(prog, log)
+            pytest.fail(log.decode())
+
+
+def test_generated_maps_follow_the_lowered_index_maps():
+    g = codegen.generate(fma_kernel().checked, _binding(fma_kernel(), [(5000,)] * 4,
+                                                         {"BLOCK": 1024}), 0)
+    # offset = (pid_0 * BLOCK + lane_0) * stride, mask against the size slot
+    assert "((pid_0 * ((i64)1024LL)) + Larr0[e]) * S.v[1]" in g.source
+    assert g.block == 256 and "constexpr int E = 4;" in g.source
+
+
+def _run(k, arrays, meta, dtype):
+    import torch
+
+    ts = [torch.from_numpy(a).cuda().to(dtype) for a in arrays]
+    out = torch.empty_like(ts[0])
+    before = backend.path_counts()["jit"]
+    k(*ts, out, **meta)
+    torch.cuda.synchronize()
+    assert backend.path_counts()["jit"] == before + 1
+    return [t.float().cpu().numpy() for t in ts], out.float().cpu().numpy()
+
+
+@pytest.mark.gpu
+def test_generic_elementwise_on_b200():
+    import torch
+
+    rng = np.random.default_rng(1)
+    xs = [rng.uniform(-1, 1, 5000).astype(np.float32) for _ in range(3)]
+    ins, out = _run(fma_kernel(), xs, {"BLOCK": 1024}, torch.float32)
+    # fp32 x*y+z on both sides; the device may contract to one fma
+    np.testing.assert_allclose(out, ins[0] * ins[1] + ins[2], rtol=1e-6, atol=1e-7)
+    for dt in (torch.float16, torch.bfloat16):
+        x = rng.uniform(-3, 3, 777).astype(np.float32)
+        (xin,), out = _run(gelu_kernel(), [x], {"BLOCK": 256}, dt)
+        ref = xin / (1 + np.exp(-1.702 * xin))
+        np.testing.assert_allclose(out, ref, rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.gpu
+def test_generic_row_reductions_on_b200():
+    import torch
+
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-4, 4, (33, 1000)).astype(np.float32)
+    (xin,), out = _run(temp_softmax_kernel(), [x], {"BLOCK": 1024}, torch.float32)
+    z = xin * 0.5
+    ref = np.exp(z - z.max(1, keepdims=True))
+    ref /= ref.sum(1, keepdims=True)
+    np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-6)
+    x = rng.uniform(-1, 1, (7, 4096)).astype(np.float32)
+    (xin,), out = _run(l2norm_kernel(), [x], {"BLOCK": 4096}, torch.float16)
+    ref = xin / np.sqrt((xin.astype(np.float64) ** 2).sum(1, keepdims=True) + 1e-6)
+    np.testing.assert_allclose(out, ref, rtol=1e-2, atol=1e-3)
