@@ -368,7 +368,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
-template <bool BF16>
+template <bool BF16, int TN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     conv_fused_kernel(const __grid_constant__ CUtensorMap wmap, const FusedParams p) {
   using namespace sm100;
@@ -435,7 +435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     }
   } else if (warp == 1) {
     if (rank == 0 && elect_one()) {
-      constexpr uint32_t idesc = idesc_f16(BF16, false, false, 256, 256);
+      constexpr uint32_t idesc = idesc_f16(BF16, false, false, 256, TN);
       int st = 0;
       uint32_t ph = 0;
       int tl = 0, wc = 0;
@@ -443,7 +443,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
         const int acc = tl & 1;
         mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * 256;
+        const uint32_t d_tmem = tmem_base + acc * TN;
         for (int cbk = 0; cbk < p.cb; ++cbk, ++wc) {
           const int wb = wc & 1;
 #if NTB_CONV_TRACE
@@ -495,7 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     uint4 v[4][4];
     auto load_chunk = [&](int t, int cbk, int g0) {
       const int n = t / tiles_img, pt = (t % tiles_img) / p.k_tiles;
-      const int q0 = pt * 256 + (int)rank * 128;
+      const int q0 = pt * TN + (int)rank * (TN / 2);
       const int c = cbk * BK + 2 * lane;
       const bool c0ok = c < p.C, c1ok = c + 1 < p.C;
       const uint16_t* src0 = xb + (int64_t)n * p.xs0 + (int64_t)c * p.xs1;
@@ -586,10 +586,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       if (tr) g_conv_trace[3000 + tl * 4 + 1] = clock64();
 #endif
       const int k0 = kt * 256 + (int)rank * 128 + ew * 32;
-      const uint32_t taddr = tmem_base + acc * 256 + ((uint32_t)(ew * 32) << 16);
+      const uint32_t taddr = tmem_base + acc * TN + ((uint32_t)(ew * 32) << 16);
       char* ybase = reinterpret_cast<char*>(p.y) + (int64_t)n * p.ys[0] * 2;
 #pragma unroll 1
-      for (int cc = 0; cc < 8; ++cc) {
+      for (int cc = 0; cc < TN / 32; ++cc) {
         uint32_t v[32];
         __syncwarp();
         tmem_ld_32x32b_x32(taddr + cc * 32, v);
@@ -603,7 +603,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
 #if NTB_CONV_TRACE
         if (tr && tl == 1) g_conv_trace[3100 + cc * 4 + 1] = clock64();
 #endif
-        const int m = pt * 256 + cc * 32 + lane;
+        const int m = pt * TN + cc * 32 + lane;
         store_chunk_rows<BF16>(xp, lane, ybase, m, p.W, p.P * p.W, p.Q, k0, p.K, p.ys);
 #if NTB_CONV_TRACE
         if (tr && tl == 1) g_conv_trace[3100 + cc * 4 + 2] = clock64();
@@ -625,9 +625,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   }
 }
 
-template <bool BF16>
+template <bool BF16, int TN>
 int launch_conv_fused(const CUtensorMap& wmap, const FusedParams& p, size_t smem, cudaStream_t s) {
-  auto k = conv_fused_kernel<BF16>;
+  auto k = conv_fused_kernel<BF16, TN>;
   static size_t attr = 0;
   if (smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -699,8 +699,14 @@ int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
     if (rc) return rc;
   }
   if (!nhwc && c.xs[3] == 1 && c.xs[2] == c.W) {
-    // fused path: the image window is staged from NCHW inside the kernel
-    const int64_t win_rows = ((128 + (c.R - 1) * c.W + (c.S - 1)) + 15) / 16 * 16;
+    // fused path: the image window is staged from NCHW inside the kernel.
+    // Pixel tile per CTA pair: 256.  (192 fits the BASELINE shape's waves
+    // better - 13.8 instead of 10.4 waves over 74 CTA pairs - but measured
+    // 197 us vs 182 us: the per-tile window fill and epilogue dominate;
+    // NTB_CONV_TN=192 selects it for experiments.)
+    static const char* tn_env = getenv("NTB_CONV_TN");
+    const int TN = tn_env && atoi(tn_env) == 192 ? 192 : 256;
+    const int64_t win_rows = ((TN / 2 + (c.R - 1) * c.W + (c.S - 1)) + 15) / 16 * 16;
     const size_t budget = 227 * 1024 - sizeof(float) * 4 * XPOSE_FLOATS - 512 - 1024;
     const size_t win_bytes = (size_t)win_rows * 128;
     int stages = STAGES;
@@ -716,7 +722,7 @@ int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
       f.N = (int)c.N; f.C = (int)c.C; f.H = (int)c.H; f.W = (int)c.W; f.K = (int)c.K;
       f.R = (int)c.R; f.S = (int)c.S; f.P = (int)c.P; f.Q = (int)c.Q;
       f.cb = (int)cdiv64(c.C, BK);
-      f.pix_tiles = (int)cdiv64((int64_t)c.P * c.W, 256);
+      f.pix_tiles = (int)cdiv64((int64_t)c.P * c.W, TN);
       f.k_tiles = (int)cdiv64(c.K, 256);
       f.win_rows = (int)win_rows;
       f.stages = stages;
@@ -727,8 +733,11 @@ int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
       f.y = c.y;
       for (int d = 0; d < 4; ++d) f.ys[d] = c.ys[d];
       const size_t smem = (size_t)stages * A_BYTES + 2 * win_bytes + 1024;
-      return bf16 ? launch_conv_fused<true>(wmap, f, smem, s)
-                  : launch_conv_fused<false>(wmap, f, smem, s);
+      if (TN == 192)
+        return bf16 ? launch_conv_fused<true, 192>(wmap, f, smem, s)
+                    : launch_conv_fused<false, 192>(wmap, f, smem, s);
+      return bf16 ? launch_conv_fused<true, 256>(wmap, f, smem, s)
+                  : launch_conv_fused<false, 256>(wmap, f, smem, s);
     }
   }
   if (!nhwc) {
