@@ -399,7 +399,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 8);
-      mbar_init(&wfull[i], 8);   // 4 window warps x 2 CTAs (arrive on CTA 0)
+      mbar_init(&wfull[i], 2);   // one publisher arrival per CTA (on CTA 0)
       mbar_init(&wempty[i], 1);
     }
     fence_barrier_init();
@@ -483,6 +483,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
         mma_commit_pair(&tfull[acc]);
       }
     }
+  } else if (warp == 3) {
+    // window publisher: waits for the 4 producer warps of this CTA, then one
+    // cluster-scope release-arrive on CTA 0's window barrier
+    int wc = 0;
+    for (int t = cid; t < total; t += ncl)
+      for (int cbk = 0; cbk < p.cb; ++cbk, ++wc) {
+        asm volatile("bar.sync %0, 160;" ::"r"(1 + (wc & 1)) : "memory");
+        if (lane == 0) mbar_arrive_cluster_rel(leader_addr(&wfull[wc & 1]));
+      }
   } else if (warp >= 8) {
     // window producers: lane = channel pair, warp = 16-pixel groups.  The
     // first chunk (<= 4 groups per warp) of the NEXT window is loaded into
@@ -553,15 +562,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     for (int t = cid; t < total; t += ncl) {
       for (int cbk = 0; cbk < p.cb; ++cbk, ++wc) {
         const int wb = wc & 1;
+#if NTB_CONV_TRACE
+        const bool trp = blockIdx.x == 0 && pw == 0 && lane == 0 && wc < 12;
+        if (trp) g_conv_trace[3200 + wc * 8 + 0] = clock64();
+#endif
         mbar_wait(&wempty[wb], ((wc >> 1) & 1) ^ 1);
+#if NTB_CONV_TRACE
+        if (trp) g_conv_trace[3200 + wc * 8 + 1] = clock64();
+#endif
         const uint32_t win_a = smem_u32(sWin + wb * WIN_BYTES);
         for (int g0 = pw; g0 < groups; g0 += 16) {
           if (g0 != pw) load_chunk(t, cbk, g0);
           store_chunk(win_a, g0);
         }
+#if NTB_CONV_TRACE
+        if (trp) g_conv_trace[3200 + wc * 8 + 2] = clock64();
+#endif
+        // hand the window to the publisher warp (named barrier 1 / 2 by
+        // window parity): the cluster-scope release it needs costs ~1k
+        // cycles and must not stall the next window's loads
         fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster_rel(leader_addr(&wfull[wb]));
+        asm volatile("bar.arrive %0, 160;" ::"r"(1 + (wc & 1)) : "memory");
+#if NTB_CONV_TRACE
+        if (trp) g_conv_trace[3200 + wc * 8 + 3] = clock64();
+#endif
         // prefetch the first chunk of the next window
         if (cbk + 1 < p.cb) load_chunk(t, cbk + 1, pw);
         else if (t + ncl < total) load_chunk(t + ncl, 0, pw);
@@ -656,6 +680,11 @@ int launch_conv_fused(const CUtensorMap& wmap, const FusedParams& p, size_t smem
     for (int tl = 0; tl < 3; ++tl)
       fprintf(stderr, "epilogue tile %d: wait@%lld got@%lld done@%lld\n", tl, h[3000 + tl * 4] - t0,
               h[3000 + tl * 4 + 1] - t0, h[3000 + tl * 4 + 2] - t0);
+    for (int w = 0; w < 12; ++w) {
+      const long long* r = h + 3200 + w * 8;
+      fprintf(stderr, "producer window %2d: start@%6lld wempty-wait %5lld stores %5lld arrive %5lld\n", w,
+              r[0] - t0, r[1] - r[0], r[2] - r[1], r[3] - r[2]);
+    }
     for (int cc = 0; cc < 8; ++cc)
       fprintf(stderr, "  tile1 chunk %d: ld@%lld xpose %lld stores %lld\n", cc, h[3100 + cc * 4] - t0,
               h[3100 + cc * 4 + 1] - h[3100 + cc * 4], h[3100 + cc * 4 + 2] - h[3100 + cc * 4 + 1]);
