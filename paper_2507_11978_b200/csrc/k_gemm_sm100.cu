@@ -79,6 +79,9 @@ struct GemmParams {
   float alpha, beta;
   int has_d;
   int tma_c;   // output written by TMA stores from a swizzled smem staging tile
+  // narrow tail: units [n_whole, n_whole + 2 * n_split) are the two 128-
+  // column halves of the last n_split tiles (M = 256, N = 128 MMAs)
+  int n_whole, n_split;
 };
 
 template <bool BF16>
@@ -343,21 +346,101 @@ constexpr int PSMEM_BYTES = PSTAGES * PSTAGE_BYTES + PSTAGE_C_BYTES + 1024;
 // then one lane issues a TMA store that clips at the output extent.  Two
 // staging buffers per warp: a buffer is rewritten only after the store that
 // read it has finished reading (bulk wait_group.read).
+// f[64] = alpha * acc (+ beta * addend) for 64 columns of one row.
+template <bool BF16>
+__device__ __forceinline__ void add_addend(const GemmParams& p, float* f, int row, int col0) {
+  if (!(p.has_d && row < p.d_m)) return;
+  const bool dvec = p.d_sn == 1 && col0 + 64 <= p.d_n && (p.d_sm % 8) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0);
+  if (dvec) {
+    const uint4* dp = reinterpret_cast<const uint4*>(
+        reinterpret_cast<const char*>(p.d) + ((int64_t)row * p.d_sm + col0) * 2);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 u = dp[q];
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float lo, hi;
+        if constexpr (BF16) {
+          __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[e]);
+          lo = __low2float(h);
+          hi = __high2float(h);
+        } else {
+          __half2 h = *reinterpret_cast<const __half2*>(&w[e]);
+          lo = __low2float(h);
+          hi = __high2float(h);
+        }
+        f[q * 8 + e * 2] += p.beta * lo;
+        f[q * 8 + e * 2 + 1] += p.beta * hi;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      const int col = col0 + i;
+      const float dv = col < p.d_n
+                           ? load_el<BF16>(p.d, (int64_t)row * p.d_sm + (int64_t)col * p.d_sn)
+                           : 0.f;
+      f[i] += p.beta * dv;
+    }
+  }
+}
+
+// One warp's 32 rows x 64 columns (row per lane, values in f) to global via
+// a 128B-swizzled staging tile and one TMA store (clipped at the output
+// extent).  `chunk` alternates the warp's two staging buffers; a buffer is
+// rewritten only after the store that read it has finished reading.
+template <bool BF16>
+__device__ __forceinline__ void store_chunk_tma(const CUtensorMap* cmap, const float* f,
+                                                uint8_t* stage, int chunk, int b, int row0,
+                                                int col0, int lane) {
+  using namespace sm100;
+  uint8_t* buf = stage + (chunk & 1) * (32 * 128);
+  if (lane == 0) bulk_wait_read<1>();
+  __syncwarp();
+  const uint32_t base = smem_u32(buf) + lane * 128;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      w[e] = BF16 ? pack_bf16(f[q * 8 + e * 2], f[q * 8 + e * 2 + 1])
+                  : pack_f16(f[q * 8 + e * 2], f[q * 8 + e * 2 + 1]);
+    const uint32_t addr = base + ((q ^ (lane & 7)) << 4);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]), "r"(w[1]),
+                 "r"(w[2]), "r"(w[3])
+                 : "memory");
+  }
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_3d(cmap, buf, col0, row0, b);
+    bulk_commit();
+  }
+}
+
+// TMA-store epilogue for one warp's 32 accumulator rows of a 256-column
+// tile: 64 columns at a time, fp32 alpha/beta epilogue, packed to 16-bit and
+// written row-per-lane into a 128B-swizzled 32 x 64 staging tile (conflict-
+// free: lanes 8 apart hit the same 16-byte chunk column only after the XOR),
+// then one lane issues a TMA store that clips at the output extent.  Two
+// staging buffers per warp.  TMEM is released as soon as the last chunk is
+// in registers.
 template <bool BF16>
 __device__ __forceinline__ void epilogue_tma(const GemmParams& p, const CUtensorMap* cmap,
                                              uint32_t taddr, uint8_t* stage, int b, int row0,
                                              int row, int col_base, uint64_t* tempty_leader_bar,
-                                             int lane) {
+                                             int lane, int nchunks = 4) {
   using namespace sm100;
 #pragma unroll 1
-  for (int cc = 0; cc < 4; ++cc) {
+  for (int cc = 0; cc < nchunks; ++cc) {
     uint32_t v[64];
     __syncwarp();
     tmem_ld_32x32b_x32(taddr + cc * 64, v);
     tmem_ld_32x32b_x32(taddr + cc * 64 + 32, v + 32);
     tmem_ld_wait();
-    if (cc == 3) {
-      // the accumulator is in registers: release TMEM to the next tile's MMAs
+    if (cc == nchunks - 1) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_addr(tempty_leader_bar));
@@ -366,67 +449,8 @@ __device__ __forceinline__ void epilogue_tma(const GemmParams& p, const CUtensor
     float f[64];
 #pragma unroll
     for (int i = 0; i < 64; ++i) f[i] = __uint_as_float(v[i]) * p.alpha;
-    if (p.has_d && row < p.d_m) {
-      const bool dvec = p.d_sn == 1 && col0 + 64 <= p.d_n && (p.d_sm % 8) == 0 &&
-                        ((reinterpret_cast<uintptr_t>(p.d) & 15) == 0);
-      if (dvec) {
-        const uint4* dp = reinterpret_cast<const uint4*>(
-            reinterpret_cast<const char*>(p.d) + ((int64_t)row * p.d_sm + col0) * 2);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const uint4 u = dp[q];
-          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float lo, hi;
-            if constexpr (BF16) {
-              __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[e]);
-              lo = __low2float(h);
-              hi = __high2float(h);
-            } else {
-              __half2 h = *reinterpret_cast<const __half2*>(&w[e]);
-              lo = __low2float(h);
-              hi = __high2float(h);
-            }
-            f[q * 8 + e * 2] += p.beta * lo;
-            f[q * 8 + e * 2 + 1] += p.beta * hi;
-          }
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const int col = col0 + i;
-          const float dv = col < p.d_n
-                               ? load_el<BF16>(p.d, (int64_t)row * p.d_sm + (int64_t)col * p.d_sn)
-                               : 0.f;
-          f[i] += p.beta * dv;
-        }
-      }
-    }
-    uint8_t* buf = stage + (cc & 1) * (32 * 128);
-    // the store issued from this buffer two chunks ago (possibly in the
-    // previous tile) must have finished reading it
-    if (lane == 0) bulk_wait_read<1>();
-    __syncwarp();
-    const uint32_t base = smem_u32(buf) + lane * 128;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      uint32_t w[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        w[e] = BF16 ? pack_bf16(f[q * 8 + e * 2], f[q * 8 + e * 2 + 1])
-                    : pack_f16(f[q * 8 + e * 2], f[q * 8 + e * 2 + 1]);
-      const uint32_t addr = base + ((q ^ (lane & 7)) << 4);
-      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]), "r"(w[1]),
-                   "r"(w[2]), "r"(w[3])
-                   : "memory");
-    }
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_3d(cmap, buf, col0, row0, b);
-      bulk_commit();
-    }
+    add_addend<BF16>(p, f, row, col0);
+    store_chunk_tma<BF16>(cmap, f, stage, cc, b, row0, col0, lane);
   }
 }
 
@@ -446,9 +470,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int tiles_per_batch = p.num_m * p.num_n;
-  const int total = tiles_per_batch * p.batch;
   const int nk = (p.K + BK - 1) / BK;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  // work units: whole 256 x 256 tiles, then the two 256 x 128 column halves
+  // of each tail tile (so the last wave keeps every CTA pair busy)
+  const int units = p.n_whole + 2 * p.n_split;
+  auto decode = [&](int u, int& t, int& half) {
+    if (u < p.n_whole) {
+      t = u; half = -1;
+    } else {
+      const int s2 = u - p.n_whole;
+      t = p.n_whole + (s2 >> 1); half = s2 & 1;
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < PSTAGES; ++i) {
@@ -478,10 +512,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     if (elect_one()) {
       int st = 0;
       uint32_t ph = 0;
-      for (int t = cid; t < total; t += ncl) {
+      for (int u = cid; u < units; u += ncl) {
+        int t, half;
+        decode(u, t, half);
         const int b = t / tiles_per_batch, r = t % tiles_per_batch;
         const int nt = r / p.num_m, mt = r % p.num_m;
-        const int row = mt * 256 + (int)rank * 128, col = nt * 256 + (int)rank * 128;
+        // narrow units: each CTA supplies 64 of the 128 columns (the TMA box
+        // still brings 128 rows / 2 chunks; the MMA reads the first 64)
+        const int row = mt * 256 + (int)rank * 128;
+        const int col = half < 0 ? nt * 256 + (int)rank * 128 : nt * 256 + half * 128 + (int)rank * 64;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[st], ph ^ 1);
           if (rank == 0) mbar_expect_tx(&full[st], 2 * PSTAGE_BYTES);
@@ -513,7 +552,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int st = 0;
       uint32_t ph = 0;
       int tl = 0;
-      for (int t = cid; t < total; t += ncl, ++tl) {
+      constexpr uint32_t idesc_n = idesc_f16(BF16, A_MN, B_MN, 256, 128);
+      for (int u = cid; u < units; u += ncl, ++tl) {
+        int t, half;
+        decode(u, t, half);
+        const uint32_t id = half < 0 ? idesc : idesc_n;
         const int acc = tl & 1;
         const uint32_t aph = (tl >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1);
@@ -530,7 +573,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                                      : umma_desc_sw128(a_addr + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + k * 2048, BK * 128, 1024)
                                      : umma_desc_sw128(b_addr + k * 32, 16, 1024);
-            mma_f16_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            mma_f16_ss_pair(d_tmem, ad, bd, id, (kb | k) != 0);
           }
           mma_commit_pair(&empty[st]);
           if (++st == PSTAGES) {
@@ -544,7 +587,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     const int ew = warp - 4;
     int tl = 0;
-    for (int t = cid; t < total; t += ncl, ++tl) {
+    for (int u = cid; u < units; u += ncl, ++tl) {
+      int t, half;
+      decode(u, t, half);
       const int b = t / tiles_per_batch, r = t % tiles_per_batch;
       const int nt = r / p.num_m, mt = r % p.num_m;
       const int acc = tl & 1;
@@ -553,7 +598,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       tc_fence_after();
       const int row0 = mt * 256 + (int)rank * 128 + ew * 32;
       const int row = row0 + lane;
-      if (p.tma_c) {
+      if (half >= 0) {
+        epilogue_tma<BF16>(p, &maps.c, tmem_base + acc * 256 + ((uint32_t)(ew * 32) << 16),
+                           sC + ew * (2 * 32 * 128), b, row0, row, nt * 256 + half * 128,
+                           &tempty[acc], lane, 2);
+      } else if (p.tma_c) {
         epilogue_tma<BF16>(p, &maps.c, tmem_base + acc * 256 + ((uint32_t)(ew * 32) << 16),
                            sC + ew * (2 * 32 * 128), b, row0, row, nt * 256, &tempty[acc], lane);
       } else {
@@ -591,6 +640,8 @@ int launch_pair(const GemmMaps& maps, const GemmParams& p, cudaStream_t s) {
 }
 
 bool ok_stride(int64_t elems) { return elems > 0 && (elems * 2) % 16 == 0; }
+
+
 
 }  // namespace
 
@@ -676,9 +727,18 @@ int gemm_sm100(const GemmDesc& g, int dtype, cudaStream_t s) {
     uint32_t box[3] = {64, 32, 1};
     p.tma_c = encode_tmap(&maps.c, dt, 3, g.c, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
   }
+  p.n_split = 0;
   if (pair) {
     p.num_m = (int)cdiv64(g.c_m, 256);
     p.num_n = (int)cdiv64(g.c_n, 256);
+    // narrow tail: if the last wave would leave more than half of the CTA
+    // pairs idle, its tiles run as two 256 x 128 halves each
+    const int64_t total = (int64_t)p.num_m * p.num_n * p.batch;
+    const int64_t pairs = sm_count() / 2;
+    const int64_t rem = total % pairs;
+    static const bool split_enabled = !getenv("NTB_GEMM_NO_SPLIT");
+    if (split_enabled && p.tma_c && total > pairs && rem > 0 && 2 * rem <= pairs) p.n_split = (int)rem;
+    p.n_whole = (int)(total - p.n_split);
     if (bf16) {
       if (a_mn) return b_mn ? launch_pair<true, true, true>(maps, p, s) : launch_pair<true, false, true>(maps, p, s);
       return b_mn ? launch_pair<false, true, true>(maps, p, s) : launch_pair<false, false, true>(maps, p, s);

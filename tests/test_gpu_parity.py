@@ -198,6 +198,35 @@ def test_mm_half(dtype, mnk):
 
 
 @pytest.mark.parametrize("dtype", DTS)
+@pytest.mark.parametrize("kernel,shape", [("mm", (2560, 4096, 1024)), ("addmm", (2560, 4096, 1024)),
+                                          ("bmm", (3, 1536, 1280, 512))])
+def test_gemm_narrow_tail(dtype, kernel, shape):
+    """Tile counts that leave the last wave of the 74 CTA pairs less than half
+    full (160 and 90 tiles) run the tail tiles as two 256 x 128 halves (N = 128
+    MMAs) on two pairs; every output element is checked, over two launches."""
+    rng = np.random.default_rng(len(shape) + shape[-1])
+    meta = {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128, "BLOCK_SIZE_K": 64}
+    if kernel == "bmm":
+        bt, m, n, k = shape
+        a = _r16(rng.uniform(-1, 1, (bt, m, k)).astype(np.float32), dtype)
+        b = _r16(rng.uniform(-1, 1, (bt, k, n)).astype(np.float32), dtype)
+        args, ref = {"input": a, "other": b}, oracle.bmm(a, b)
+    else:
+        m, n, k = shape
+        a = _r16(rng.uniform(-1, 1, (m, k)).astype(np.float32), dtype)
+        b = _r16(rng.uniform(-1, 1, (k, n)).astype(np.float32), dtype)
+        if kernel == "mm":
+            args, ref = {"input": a, "other": b}, oracle.mm(a, b)
+        else:
+            inp = _r16(rng.uniform(-1, 1, (m, n)).astype(np.float32), dtype)
+            args = {"input": inp, "mat1": a, "mat2": b, "beta": 0.5, "alpha": -1.5}
+            ref = oracle.addmm(inp, a, b, 0.5, -1.5)
+    for _ in range(2):
+        got = _run(kernel, args, meta, dtype)
+        _close(got, ref, rtol=1e-2, atol=3e-2)
+
+
+@pytest.mark.parametrize("dtype", DTS)
 def test_mm_transposed_operands(dtype):
     rng = np.random.default_rng(3)
     m, n, k = 384, 256, 512
