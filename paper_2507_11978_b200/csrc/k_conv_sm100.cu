@@ -347,6 +347,7 @@ struct FusedParams {
   int N, C, H, W, K, R, S, P, Q;
   int cb, pix_tiles, k_tiles;
   int win_rows, stages;
+  int n_whole, n_split;   // whole tiles, then 2 x n_split half-width tail units
   const void* x;
   int64_t xs0, xs1;   // batch / channel strides (elements); planes are contiguous H*W runs
   int vec;            // 16-byte image loads allowed
@@ -387,8 +388,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   const uint32_t rank = cluster_rank();
   const int RS = p.R * p.S;
   const int tiles_img = p.pix_tiles * p.k_tiles;
-  const int total = tiles_img * p.N;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  // work units: whole tiles (TN pixels), then the two TN/2-pixel halves of
+  // each tail tile (N = TN/2 MMAs) so the last wave keeps every pair busy
+  const int total = p.n_whole + 2 * p.n_split;
+  struct Unit { int n, pt, kt, pix0, npix; };
+  auto decode = [&](int u) {
+    Unit w;
+    int t = u, off = 0, np = TN;
+    if (u >= p.n_whole) {
+      const int s2 = u - p.n_whole;
+      t = p.n_whole + (s2 >> 1);
+      off = (s2 & 1) * (TN / 2);
+      np = TN / 2;
+    }
+    w.n = t / tiles_img;
+    const int rr = t % tiles_img;
+    w.pt = rr / p.k_tiles;
+    w.kt = rr % p.k_tiles;
+    w.pix0 = w.pt * TN + off;
+    w.npix = np;
+    return w;
+  };
   const int stages = p.stages;
 
   if (threadIdx.x == 0) {
@@ -418,8 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       int st = 0;
       uint32_t ph = 0;
       for (int t = cid; t < total; t += ncl) {
-        const int rr = t % tiles_img;
-        const int kt = rr % p.k_tiles;
+        const int kt = decode(t).kt;
         const int krow = kt * 256 + (int)rank * 128;
         for (int cbk = 0; cbk < p.cb; ++cbk)
           for (int rs = 0; rs < RS; ++rs) {
@@ -435,11 +455,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     }
   } else if (warp == 1) {
     if (rank == 0 && elect_one()) {
-      constexpr uint32_t idesc = idesc_f16(BF16, false, false, 256, TN);
+      constexpr uint32_t idesc_w = idesc_f16(BF16, false, false, 256, TN);
+      constexpr uint32_t idesc_h = idesc_f16(BF16, false, false, 256, TN / 2);
       int st = 0;
       uint32_t ph = 0;
       int tl = 0, wc = 0;
       for (int t = cid; t < total; t += ncl, ++tl) {
+        const uint32_t idesc = decode(t).npix == TN ? idesc_w : idesc_h;
         const int acc = tl & 1;
         mbar_wait(&tempty[acc], ((tl >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -499,12 +521,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
     // latency is off the critical path; only the stores wait for the buffer.
     const int pw = warp - 8;
     const int HW = p.H * p.W;
-    const int groups = p.win_rows / 16;
+    const int halo = (p.R - 1) * p.W + (p.S - 1);
     const uint16_t* xb = reinterpret_cast<const uint16_t*>(p.x);
     uint4 v[4][4];
     auto load_chunk = [&](int t, int cbk, int g0) {
-      const int n = t / tiles_img, pt = (t % tiles_img) / p.k_tiles;
-      const int q0 = pt * TN + (int)rank * (TN / 2);
+      const Unit w = decode(t);
+      const int n = w.n;
+      const int q0 = w.pix0 + (int)rank * (w.npix / 2);
+      const int groups = (w.npix / 2 + halo + 15) / 16;
       const int c = cbk * BK + 2 * lane;
       const bool c0ok = c < p.C, c1ok = c + 1 < p.C;
       const uint16_t* src0 = xb + (int64_t)n * p.xs0 + (int64_t)c * p.xs1;
@@ -536,7 +560,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
         }
       }
     };
-    auto store_chunk = [&](uint32_t win_a, int g0) {
+    auto store_chunk = [&](uint32_t win_a, int g0, int groups) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int g = g0 + 4 * u;
@@ -571,9 +595,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
         if (trp) g_conv_trace[3200 + wc * 8 + 1] = clock64();
 #endif
         const uint32_t win_a = smem_u32(sWin + wb * WIN_BYTES);
+        const int groups = (decode(t).npix / 2 + halo + 15) / 16;
         for (int g0 = pw; g0 < groups; g0 += 16) {
           if (g0 != pw) load_chunk(t, cbk, g0);
-          store_chunk(win_a, g0);
+          store_chunk(win_a, g0, groups);
         }
 #if NTB_CONV_TRACE
         if (trp) g_conv_trace[3200 + wc * 8 + 2] = clock64();
@@ -597,8 +622,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
 
     int tl = 0;
     for (int t = cid; t < total; t += ncl, ++tl) {
-      const int n = t / tiles_img, rr = t % tiles_img;
-      const int pt = rr / p.k_tiles, kt = rr % p.k_tiles;
+      const Unit w = decode(t);
+      const int n = w.n, kt = w.kt;
       const int acc = tl & 1;
 #if NTB_CONV_TRACE
       const bool tr = blockIdx.x == 0 && tl < 3 && ew == 0 && lane == 0;
@@ -613,7 +638,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
       const uint32_t taddr = tmem_base + acc * TN + ((uint32_t)(ew * 32) << 16);
       char* ybase = reinterpret_cast<char*>(p.y) + (int64_t)n * p.ys[0] * 2;
 #pragma unroll 1
-      for (int cc = 0; cc < TN / 32; ++cc) {
+      for (int cc = 0; cc < w.npix / 32; ++cc) {
         uint32_t v[32];
         __syncwarp();
         tmem_ld_32x32b_x32(taddr + cc * 32, v);
@@ -627,7 +652,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
 #if NTB_CONV_TRACE
         if (tr && tl == 1) g_conv_trace[3100 + cc * 4 + 1] = clock64();
 #endif
-        const int m = pt * TN + cc * 32 + lane;
+        const int m = w.pix0 + cc * 32 + lane;
         store_chunk_rows<BF16>(xp, lane, ybase, m, p.W, p.P * p.W, p.Q, k0, p.K, p.ys);
 #if NTB_CONV_TRACE
         if (tr && tl == 1) g_conv_trace[3100 + cc * 4 + 2] = clock64();
@@ -754,6 +779,16 @@ int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
       f.pix_tiles = (int)cdiv64((int64_t)c.P * c.W, TN);
       f.k_tiles = (int)cdiv64(c.K, 256);
       f.win_rows = (int)win_rows;
+      {
+        // narrow tail (as in the GEMM): last-wave tiles split into two
+        // half-width units when more than half the CTA pairs would idle
+        const int64_t total = (int64_t)c.N * f.pix_tiles * f.k_tiles;
+        const int64_t pairs = sm_count() / 2;
+        const int64_t rem = total % pairs;
+        static const bool split = !getenv("NTB_CONV_NO_SPLIT");
+        f.n_split = (split && total > pairs && rem > 0 && 2 * rem <= pairs) ? (int)rem : 0;
+        f.n_whole = (int)(total - f.n_split);
+      }
       f.stages = stages;
       f.x = c.x;
       f.xs0 = c.xs[0];

@@ -272,7 +272,7 @@ def test_bmm_half(dtype, bmnk):
 @pytest.mark.parametrize("shape", [(1, 2, 5, 5, 3, 3, 3), (2, 16, 12, 10, 32, 3, 3),
                                    (2, 64, 30, 30, 128, 3, 3), (4, 256, 56, 56, 256, 3, 3),
                                    (3, 100, 17, 23, 320, 5, 5), (9, 64, 40, 40, 64, 1, 1),
-                                   (20, 96, 28, 28, 192, 3, 3)])
+                                   (20, 96, 28, 28, 192, 3, 3), (8, 64, 56, 56, 64, 3, 3)])
 def test_conv2d_half(dtype, shape):
     n, c, h, w, k, r, s = shape
     rng = np.random.default_rng(c)
