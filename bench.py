@@ -486,10 +486,35 @@ def headline(args, n_gpus, rank, pk):
     e2e_ms = _max_over_ranks(e0.elapsed_time(e1), n_gpus) / args.steps
     h2d = 2 * R * C * 2 + C * 2
     d2h = 2 * R * C * 2
+    # PCIe ceiling for the same bytes: the step's H2D and D2H copies alone,
+    # concurrently on two streams (no kernels) - what e2e is bound by
+    def copies_only(n):
+        for i in range(n):
+            b_ = i % nbuf
+            with torch.cuda.stream(s_in):
+                dx[b_].copy_(hx[b_], non_blocking=True)
+                dxb[b_].copy_(hxb[b_], non_blocking=True)
+            with torch.cuda.stream(s_out):
+                hy[b_].copy_(dy[b_], non_blocking=True)
+                hz[b_].copy_(dz[b_], non_blocking=True)
+
+    copies_only(2)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(s_in)
+    s_out.wait_stream(s_in)
+    copies_only(args.steps)
+    s_in.wait_stream(s_out)
+    c1.record(s_in)
+    torch.cuda.synchronize()
+    pcie_ms = c0.elapsed_time(c1) / args.steps
     e2e = {"value": round(n_gpus * step_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": round(e2e_ms, 4),
-           "how": "public launchers, pinned host buffers, H2D/compute/D2H on 3 streams"}
+           "how": "public launchers, pinned host buffers, H2D/compute/D2H on 3 streams",
+           "pcie_ceiling": {"what": "the same H2D + D2H copies per step, concurrent, no kernels",
+                            "ms_per_step": round(pcie_ms, 4),
+                            "e2e_frac_of_ceiling": round(pcie_ms / e2e_ms, 4)}}
 
     dom, dom_ms, dom_units = ("softmax", sm_ms, 2 * R * C * 2) if sm_ms >= rms_ms else \
         ("rms_norm", rms_ms, 2 * R * C * 2 + C * 2)
