@@ -116,6 +116,9 @@ __global__ void __launch_bounds__(256) row_vec_kernel(const T* __restrict__ in, 
 // bandwidth.  The warp reduces its row out of shared memory (warp shuffles,
 // fp32) and writes the result with 128-bit streaming stores.
 constexpr int kStreamWarps = 16;
+#ifndef NTB_ROWS_REG
+#define NTB_ROWS_REG 1
+#endif
 constexpr int kStreamMaxStages = 8;
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -225,6 +228,79 @@ __device__ __forceinline__ void rms_row_f16(const uint4* buf, const uint4* wv, _
   }
 }
 
+// Register-resident variants for rows of exactly 32 * VPL packs (4096 fp16
+// columns = VPL 16): the row is read from shared memory ONCE into registers
+// (64 registers per lane) and the max / exp / sum / scale passes run there.
+template <int VPL>
+__device__ __forceinline__ void softmax_row_f16_reg(const uint4* buf, __half* dst, int lane) {
+  uint4 v[VPL];
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) v[u] = buf[lane + 32 * u];
+  __half2 mx = __float2half2_rn(-INFINITY);
+#pragma unroll
+  for (int u = 0; u < VPL; ++u)
+    mx = __hmax2(mx, __hmax2(__hmax2(u2h(v[u].x), u2h(v[u].y)), __hmax2(u2h(v[u].z), u2h(v[u].w))));
+  float m = fmaxf(__low2float(mx), __high2float(mx));
+  m = warp_max(m);
+  const __half2 l2e = __float2half2_rn(1.4426950408889634f);
+  const __half2 m2 = __float2half2_rn(m);
+  float sum = 0.f;
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) {
+    uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+    __half2 acc = __float2half2_rn(0.f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __half2 e = h2exp2(__hmul2(__hsub2(u2h(w[k]), m2), l2e));
+      acc = __hadd2(acc, e);
+      w[k] = h2u(e);
+    }
+    v[u] = make_uint4(w[0], w[1], w[2], w[3]);
+    const float2 a = __half22float2(acc);
+    sum += a.x + a.y;
+  }
+  const __half2 inv = __float2half2_rn(1.0f / warp_sum(sum));
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) {
+    const uint4 o = make_uint4(h2u(__hmul2(u2h(v[u].x), inv)), h2u(__hmul2(u2h(v[u].y), inv)),
+                               h2u(__hmul2(u2h(v[u].z), inv)), h2u(__hmul2(u2h(v[u].w), inv)));
+    st_stream(dst + (int64_t)(lane + 32 * u) * 8, o);
+  }
+}
+
+template <int VPL>
+__device__ __forceinline__ void rms_row_f16_reg(const uint4* buf, const uint4* wv, __half* dst,
+                                                int cols, int lane) {
+  uint4 v[VPL];
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) v[u] = buf[lane + 32 * u];
+  float ss = 0.f;
+  const __half2 sc = __float2half2_rn(1.0f / 1024.0f);
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) {
+    const __half2 a0 = __hmul2(u2h(v[u].x), sc), a1 = __hmul2(u2h(v[u].y), sc);
+    const __half2 a2 = __hmul2(u2h(v[u].z), sc), a3 = __hmul2(u2h(v[u].w), sc);
+    __half2 acc = __hmul2(a0, a0);
+    acc = __hfma2(a1, a1, acc);
+    acc = __hfma2(a2, a2, acc);
+    acc = __hfma2(a3, a3, acc);
+    const float2 a = __half22float2(acc);
+    ss += a.x + a.y;
+  }
+  ss *= 1048576.0f;
+  const float rinv = 1.0f / sqrtf(warp_sum(ss) / (float)cols + kRmsEps);
+  const __half2 r2 = __float2half2_rn(rinv);
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) {
+    const uint4 g = wv[lane + 32 * u];
+    const uint4 o = make_uint4(h2u(__hmul2(__hmul2(u2h(v[u].x), r2), u2h(g.x))),
+                               h2u(__hmul2(__hmul2(u2h(v[u].y), r2), u2h(g.y))),
+                               h2u(__hmul2(__hmul2(u2h(v[u].z), r2), u2h(g.z))),
+                               h2u(__hmul2(__hmul2(u2h(v[u].w), r2), u2h(g.w))));
+    st_stream(dst + (int64_t)(lane + 32 * u) * 8, o);
+  }
+}
+
 template <typename T, bool kSoftmax>
 __global__ void __launch_bounds__(kStreamWarps * 32, 1)
     row_stream_kernel(const T* __restrict__ in, int64_t in_rs, const T* __restrict__ w,
@@ -270,8 +346,14 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
     const uint4* buf = reinterpret_cast<const uint4*>(wbase + (size_t)s * row_pad);
     T* dst = out + r * out_rs;
     if constexpr (std::is_same<T, __half>::value) {
-      if (kSoftmax) softmax_row_f16(buf, dst, n_vec, lane);
-      else rms_row_f16(buf, reinterpret_cast<const uint4*>(wsh), dst, n_vec, cols, lane);
+      if (n_vec == 32 * 16 && NTB_ROWS_REG) {
+        if (kSoftmax) softmax_row_f16_reg<16>(buf, dst, lane);
+        else rms_row_f16_reg<16>(buf, reinterpret_cast<const uint4*>(wsh), dst, cols, lane);
+      } else if (kSoftmax) {
+        softmax_row_f16(buf, dst, n_vec, lane);
+      } else {
+        rms_row_f16(buf, reinterpret_cast<const uint4*>(wsh), dst, n_vec, cols, lane);
+      }
     } else if (kSoftmax) {
       // pass 1: row max; pass 2: e = exp(x - m) written back in place (fp16
       // for 16-bit rows, fp32 for fp32 rows) + row sum; pass 3: e / sum.
