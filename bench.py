@@ -327,9 +327,19 @@ def time_work(work, steps, warmup, n_gpus):
     t1.record(stream)
     _barrier(n_gpus)
     total = t0.elapsed_time(t1)
+    # clocks under this kernel's own load: the same graph replayed back to
+    # back for ~0.3 s while NVML samples SM clock and throttle reasons
+    reps = max(2, int(0.3 / max(total * 1e-3, 1e-6)))
+    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for _ in range(reps):
+            g.replay()
+        torch.cuda.synchronize()
+    # let the power-capped clock recover before the next kernel is timed
+    # (the window above is a sustained load; the timings are bursts)
+    time.sleep(1.0)
     del g, sets
     torch.cuda.empty_cache()
-    return total / steps, total, launches
+    return total / steps, total, launches, clk.summary()
 
 
 def _roofline(work, ms, pk, traffic):
@@ -654,11 +664,17 @@ def main():
         for key, wk in works.items():
             try:
                 steps = 3 if key in ("sdpa", "sdpa_rope", "rope+sdpa") else args.kernel_steps
-                ms, total, launches = time_work(wk, steps, 2, n_gpus)
+                ms, total, launches, clk = time_work(wk, steps, 2, n_gpus)
                 ms = _max_over_ranks(ms, n_gpus)
+                roof = _roofline(wk, ms, pk, traffic.get(key))
+                if wk.bound == "tensor" and pk.get("tc_sus"):
+                    # the same achieved rate against the sustained (power-
+                    # capped) tensor peak, for reading alongside sm_mhz
+                    roof["frac_of_sustained"] = round(roof["achieved"] / pk["tc_sus"], 4)
                 kernels[key] = {"workload": wk.name, "ms": round(ms, 5),
                                 "launches": launches,
-                                "roofline": _roofline(wk, ms, pk, traffic.get(key)),
+                                "roofline": roof,
+                                "clocks_under_load": clk,
                                 "note": wk.note}
             except Exception as e:  # report, never hide
                 kernels[key] = {"workload": wk.name, "error": f"{type(e).__name__}: {e}"}
