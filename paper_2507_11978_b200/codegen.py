@@ -22,13 +22,16 @@ Execution model (one CTA per program, the reference's program = one tile):
   ``%`` (symexpr.py:31-161), float math is fp32, loads/stores convert from /
   to the tensor dtype (f32, f16, bf16).
 
-Supported application IR: Let / Assign / Accumulate / Store at the top level;
-Load with constant nest indices; + - * / max min; exp, sqrt, rsqrt, log,
-sigmoid, neg, abs, tanh, relu; numeric constants; ShapeOf; Zeros; Reduce
-(max / sum) over the WHOLE tile (every other lane axis of extent 1, e.g.
-softmax / rms_norm-style rows).  Loops (ForRange) and Dot are not generated:
-those families have native tensor-core kernels, and anything else raises
-UnsupportedSpecError with the reason.
+Supported application IR: Let / Store at the top level, Assign / Accumulate
+anywhere; ``for`` loops over a nest (ForRange) with loads indexed by the loop
+variable or constants; + - * / max min; exp, sqrt, rsqrt, log, sigmoid, neg,
+abs, tanh, relu; numeric constants; ShapeOf; Zeros; Reduce (max / sum) over
+the WHOLE tile (every other lane axis of extent 1, e.g. softmax / rms_norm-
+style rows); Dot of two (transposed) 2-D operand tiles into the 2-D output
+tile - both operands staged in shared memory, fp32 FMA accumulation on the
+CUDA cores (the paper's contractions run on the native tcgen05 kernels; this
+is the path for OTHER contractions, e.g. a matmul with a fused epilogue).
+Anything else raises UnsupportedSpecError with the reason.
 """
 
 from __future__ import annotations
@@ -40,7 +43,7 @@ from dataclasses import dataclass
 from . import symbolic as se
 from .arrange import Grid
 from .spec import (Accumulate, Assign, BinOp, ConstF, Dot, ForRange, IConst, Let, Load, Local,
-                   Reduce, ShapeOf, Store, UnOp, Zeros)
+                   Reduce, ShapeOf, Store, UnOp, Var, Zeros)
 
 
 class CodegenError(Exception):
@@ -127,22 +130,34 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
     spec = checked.spec
     tensors = [p for p in spec.params if p.rank >= 1]
     scalars = [p for p in spec.params if p.rank == 0]
+    tnames = [t.name for t in tensors]
     maps = {p.name: checked.index_maps[p.name] for p in tensors}
 
     def ev(e) -> int:
         return int(se.evaluate(se.from_any(e), binding))
 
-    # lane universe: per-axis maximum; each parameter is 1 or the maximum there
-    ndim = {len(m.lane_sizes) for m in maps.values()}
-    if len(ndim) != 1:
-        raise CodegenError("parameters with lane tiles of different rank")
-    nd = ndim.pop()
     ext = {n: [ev(s) for s in m.lane_sizes] for n, m in maps.items()}
-    uni = [max(ext[n][j] for n in ext) for j in range(nd)]
-    for n, e in ext.items():
-        for j in range(nd):
-            if e[j] not in (1, uni[j]):
-                raise CodegenError(f"lane tile of {n!r} ({e}) does not broadcast to {uni}")
+
+    # the element universe is the lane tile of the stored parameter(s)
+    def stores(stmts):
+        for st in stmts:
+            if isinstance(st, Store):
+                yield st
+            elif isinstance(st, ForRange):
+                yield from stores(st.body)
+    stored_params = [st.param for st in stores(spec.application)]
+    if not stored_params:
+        raise CodegenError("the application stores nothing")
+    uni = ext[stored_params[0]]
+    for n in stored_params:
+        if ext[n] != uni:
+            raise CodegenError("stored parameters with different lane tiles")
+    nd = len(uni)
+
+    def bcast_ok(n):
+        e = ext[n]
+        return len(e) == nd and all(e[j] in (1, uni[j]) for j in range(nd))
+
     lane_total = math.prod(uni) if uni else 1
     if lane_total < 1:
         raise CodegenError("empty lane tile")
@@ -150,40 +165,6 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
     per_thread = math.ceil(lane_total / block)
     if per_thread > 64:
         raise CodegenError(f"lane tile of {lane_total} elements is too large for one CTA")
-
-    # statement kinds (element vs whole-tile scalar) ---------------------------
-    kind: dict = {}
-
-    def ekind(x) -> str:
-        if isinstance(x, Load):
-            for n in x.nests:
-                if not isinstance(n, IConst):
-                    raise CodegenError("loads with loop-variable nest indices are not generated")
-            return "scalar" if spec.param(x.param).rank == 0 else "elem"
-        if isinstance(x, Local):
-            return kind[x.name]
-        if isinstance(x, (ConstF, ShapeOf)):
-            return "scalar"
-        if isinstance(x, Zeros):
-            return "elem" if x.shape else "scalar"
-        if isinstance(x, BinOp):
-            if x.op not in _BIN:
-                raise CodegenError(f"binary op {x.op!r}")
-            return "elem" if "elem" in (ekind(x.a), ekind(x.b)) else "scalar"
-        if isinstance(x, UnOp):
-            if x.op not in _UN:
-                raise CodegenError(f"unary op {x.op!r}")
-            return ekind(x.a)
-        if isinstance(x, Reduce):
-            if x.op not in ("max", "sum"):
-                raise CodegenError(f"reduction {x.op!r}")
-            if any(uni[j] != 1 for j in range(nd) if j != x.axis):
-                raise CodegenError("only whole-tile reductions are generated")
-            ekind(x.a)
-            return "scalar"
-        if isinstance(x, Dot):
-            raise CodegenError("dot products run on the native tensor-core kernels only")
-        raise CodegenError(f"expression {type(x).__name__}")
 
     slot_names = []
     for p in tensors:
@@ -206,51 +187,113 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
                 total=se.lit(1), checks=())
     pidc = grid.pid_components(se.var("pid"))
 
-    body = []
+    kind: dict = {}
+    loopvar: dict = {}            # IR loop variable -> C variable
+    body: list = []
+    shared_decls: list = []
+    smem_bytes = [0]
     tmp = [0]
+    ind = ["  "]
 
     def fresh():
         tmp[0] += 1
         return f"t{tmp[0]}"
 
-    def load_code(x: Load, e: str) -> str:
-        """Emit the offset/mask/load of element ``e`` of parameter x.param; returns the
-        float variable holding the value."""
-        m = maps[x.param]
-        nests = {f"nest_{k}": int(n.value) for k, n in enumerate(x.nests)}
-        bcast = ext[x.param]
+    def emit(line):
+        body.append(ind[0] + line)
+
+    def nest_c(n):
+        if isinstance(n, IConst):
+            return f"((i64){int(n.value)}LL)"
+        if isinstance(n, Var):
+            if n.name not in loopvar:
+                raise CodegenError(f"unknown loop variable {n.name!r}")
+            return loopvar[n.name]
+        raise CodegenError("nest index must be a constant or a loop variable")
+
+    def map_sym(param, nests, lane_expr):
+        """Renderer for the symbols of ``param``'s map: nest_k from ``nests``,
+        lane_j from ``lane_expr(j)``."""
+        nc = {f"nest_{k}": nest_c(n) for k, n in enumerate(nests)}
 
         def sym(name):
             if name.startswith("lane_"):
-                j = int(name[5:])
-                return "((i64)0)" if bcast[j] == 1 and uni[j] != 1 else f"L{j}_{e}"
+                return lane_expr(int(name[5:]))
             if name.startswith("nest_"):
-                return f"((i64){nests.get(name, 0)}LL)"
+                return nc.get(name, "((i64)0LL)")
             return gsym(name)
+        return sym
 
-        v = fresh()
+    def off_mask(param, sym):
+        m = maps[param]
         off = _render(m.offset, sym)
         conds = [f"(({_render(lhs, sym)}) >= 0 && ({_render(lhs, sym)}) < ({_render(b, sym)}))"
                  for lhs, b in m.mask]
-        mask = " && ".join(conds) if conds else "true"
-        pi = [t.name for t in tensors].index(x.param)
-        body.append(f"  float {v} = ({mask}) ? to_f(p{pi}[{off}]) : {float(x.other)!r}f;"
-                    .replace("inff", "INFINITY").replace("-INFINITY", "(-INFINITY)"))
-        return v
+        return off, (" && ".join(conds) if conds else "true")
 
-    def expr(x, e: str) -> str:
-        """C float expression of x at element index variable e (elem) or scalar."""
+    def fill(v):
+        v = float(v)
+        if math.isinf(v):
+            return "(-INFINITY)" if v < 0 else "INFINITY"
+        return f"{v!r}f"
+
+    # -- kinds ---------------------------------------------------------------
+    def ekind(x) -> str:
+        if isinstance(x, Load):
+            if spec.param(x.param).rank == 0:
+                return "scalar"
+            if not bcast_ok(x.param):
+                raise CodegenError(f"{x.param!r} has a lane tile {ext[x.param]} that is neither "
+                                   f"the output tile {uni} nor a dot operand")
+            for n in x.nests:
+                nest_c(n)
+            return "elem"
+        if isinstance(x, Local):
+            if x.name not in kind:
+                raise CodegenError(f"undefined local {x.name!r}")
+            return kind[x.name]
+        if isinstance(x, (ConstF, ShapeOf)):
+            return "scalar"
+        if isinstance(x, Zeros):
+            return "elem" if x.shape else "scalar"
+        if isinstance(x, BinOp):
+            if x.op not in _BIN:
+                raise CodegenError(f"binary op {x.op!r}")
+            return "elem" if "elem" in (ekind(x.a), ekind(x.b)) else "scalar"
+        if isinstance(x, UnOp):
+            if x.op not in _UN:
+                raise CodegenError(f"unary op {x.op!r}")
+            return ekind(x.a)
+        if isinstance(x, Reduce):
+            if x.op not in ("max", "sum"):
+                raise CodegenError(f"reduction {x.op!r}")
+            if any(uni[j] != 1 for j in range(nd) if j != x.axis):
+                raise CodegenError("only whole-tile reductions are generated")
+            ekind(x.a)
+            return "scalar"
+        if isinstance(x, Dot):
+            return "elem"
+        raise CodegenError(f"expression {type(x).__name__}")
+
+    # -- element expressions -------------------------------------------------
+    def elem_lane(param):
+        e = ext[param]
+        return lambda j: "((i64)0)" if e[j] == 1 and uni[j] != 1 else f"Larr{j}[e]"
+
+    def expr(x) -> str:
+        """C float expression of x for element e (inside an element loop)."""
         if isinstance(x, Load):
             if spec.param(x.param).rank == 0:
                 return f"s_{x.param}"
-            return load_code(x, e)
+            off, mask = off_mask(x.param, map_sym(x.param, x.nests, elem_lane(x.param)))
+            v = fresh()
+            emit(f"  const float {v} = ({mask}) ? to_f(p{tnames.index(x.param)}[{off}]) : "
+                 f"{fill(x.other)};")
+            return v
         if isinstance(x, Local):
-            return f"v_{x.name}[{e}]" if kind[x.name] == "elem" else f"v_{x.name}"
+            return f"v_{x.name}[e]" if kind[x.name] == "elem" else f"v_{x.name}"
         if isinstance(x, ConstF):
-            v = float(x.value)
-            if math.isinf(v):
-                return "(-INFINITY)" if v < 0 else "INFINITY"
-            return f"{v!r}f"
+            return fill(x.value)
         if isinstance(x, Zeros):
             return "0.0f"
         if isinstance(x, ShapeOf):
@@ -258,129 +301,190 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
             if x.of == "source":
                 return f"((float){gsym(f'{x.param}_size_{x.dim}')})"
             if x.of == "nest":
-                return f"{float(ev(m.nest_sizes[x.dim]))!r}f"
+                return f"((float){_render(m.nest_sizes[x.dim], gsym)})"
             return f"{float(ev(m.lane_sizes[x.dim]))!r}f"
         if isinstance(x, BinOp):
-            return _BIN[x.op].format(a=expr(x.a, e), b=expr(x.b, e))
+            return _BIN[x.op].format(a=expr(x.a), b=expr(x.b))
         if isinstance(x, UnOp):
-            return _UN[x.op].format(a=expr(x.a, e))
+            return _UN[x.op].format(a=expr(x.a))
         raise CodegenError(f"expression {type(x).__name__}")
 
-    def elem_loop(stmt_fn):
-        body.append(f"  #pragma unroll\n  for (int e = 0; e < E; ++e) {{")
-        body.append("    if (!V[e]) continue;")
-        stmt_fn("e")
-        body.append("  }")
+    def elem_loop(fn):
+        emit("#pragma unroll")
+        emit("for (int e = 0; e < E; ++e) {")
+        emit("  if (!V[e]) continue;")
+        ind[0] += "  "
+        fn()
+        ind[0] = ind[0][:-2]
+        emit("}")
 
+    # -- whole-tile reductions and dot products (hoisted) --------------------
     def reduce_code(x: Reduce) -> str:
         r = fresh()
         ident = "(-INFINITY)" if x.op == "max" else "0.0f"
         comb = "fmaxf({a}, {b})" if x.op == "max" else "({a} + {b})"
-        body.append(f"  float {r} = {ident};")
-        saved = len(body)
-        elem_loop(lambda e: body.append(
-            f"    {r} = {comb.format(a=r, b=expr(x.a, e))};"))
-        del saved
-        body.append(f"  {r} = block_reduce_{x.op}({r}, red);")
+        inner = hoist(x.a)
+        emit(f"float {r} = {ident};")
+        elem_loop(lambda: emit(f"  {r} = {comb.format(a=r, b=expr(inner))};"))
+        emit(f"{r} = block_reduce_{x.op}({r}, red);")
         return r
 
-    def scalar_expr(x) -> str:
-        """Scalar-kind expression: reductions evaluated first."""
-        if isinstance(x, Reduce):
-            return reduce_code(x)
-        if isinstance(x, BinOp):
-            return _BIN[x.op].format(a=scalar_expr(x.a), b=scalar_expr(x.b))
-        if isinstance(x, UnOp):
-            return _UN[x.op].format(a=scalar_expr(x.a))
-        return expr(x, "0")
+    def operand(x):
+        """(Load, transposed) of a dot operand."""
+        if isinstance(x, UnOp) and x.op == "trans" and isinstance(x.a, Load):
+            return x.a, True
+        if isinstance(x, Load):
+            return x, False
+        raise CodegenError("dot operands must be (transposed) loads")
+
+    def dot_code(x: Dot) -> str:
+        if nd != 2:
+            raise CodegenError("dot needs a 2-D output tile")
+        (la, ta), (lb, tb) = operand(x.a), operand(x.b)
+        ea, eb = ext[la.param], ext[lb.param]
+        if len(ea) != 2 or len(eb) != 2:
+            raise CodegenError("dot operands must be 2-D tiles")
+        M, K = (ea[1], ea[0]) if ta else (ea[0], ea[1])
+        K2, N = (eb[1], eb[0]) if tb else (eb[0], eb[1])
+        if K != K2 or M != uni[0] or N != uni[1]:
+            raise CodegenError(f"dot shapes {ea}{'T' if ta else ''} x {eb}{'T' if tb else ''} "
+                               f"do not produce the output tile {uni}")
+        elt = 4 if dtype == 0 else 2
+        need = (M * K + K * N) * elt
+        if smem_bytes[0] + need > 46 * 1024:
+            raise CodegenError(f"dot operand tiles of {need} bytes exceed the generic path's "
+                               "shared-memory budget")
+        smem_bytes[0] += need
+        sa, sb, t = fresh(), fresh(), fresh()
+        shared_decls.append(f"  __shared__ T s{sa}[{M * K}];")
+        shared_decls.append(f"  __shared__ T s{sb}[{K * N}];")
+
+        def stage(ld, trans, rows, cols, dst):
+            # dst[r * cols + c] <- operand element (r, c) (transposed view if trans)
+            lane = (lambda j: "(i64)c_" if j == 0 else "(i64)r_") if trans else \
+                   (lambda j: "(i64)r_" if j == 0 else "(i64)c_")
+            off, mask = off_mask(ld.param, map_sym(ld.param, ld.nests, lane))
+            pi = tnames.index(ld.param)
+            emit(f"for (int q_ = threadIdx.x; q_ < {rows * cols}; q_ += NT) {{")
+            emit(f"  const int r_ = q_ / {cols}, c_ = q_ % {cols};")
+            emit(f"  s{dst}[q_] = ({mask}) ? p{pi}[{off}] : from_f<T>({fill(ld.other)});")
+            emit("}")
+
+        emit("__syncthreads();")
+        stage(la, ta, M, K, sa)
+        stage(lb, tb, K, N, sb)
+        emit("__syncthreads();")
+        emit(f"float {t}[E];")
+
+        def comp():
+            emit(f"  const int i_ = (int)Larr0[e], j_ = (int)Larr1[e];")
+            emit(f"  float acc_ = 0.0f;")
+            emit(f"  #pragma unroll 8")
+            emit(f"  for (int k_ = 0; k_ < {K}; ++k_)")
+            emit(f"    acc_ = fmaf(to_f(s{sa}[i_ * {K} + k_]), to_f(s{sb}[k_ * {N} + j_]), acc_);")
+            emit(f"  {t}[e] = acc_;")
+        elem_loop(comp)
+        kind[t] = "elemtmp"
+        return t
 
     def hoist(x):
-        """Replace whole-tile reductions inside an element expression by scalars."""
+        """Evaluate reductions and dots first; return an element expression."""
         if isinstance(x, Reduce):
-            return Local(_hoisted(x))
+            name = fresh()
+            emit(f"const float v_{name} = {reduce_code(x)};")
+            kind[name] = "scalar"
+            return Local(name)
+        if isinstance(x, Dot):
+            t = dot_code(x)
+            kind[t] = "elem"
+            emit(f"float* v_{t} = {t};")
+            return Local(t)
         if isinstance(x, BinOp):
             return BinOp(x.op, hoist(x.a), hoist(x.b))
         if isinstance(x, UnOp):
             return UnOp(x.op, hoist(x.a))
         return x
 
-    def _hoisted(x):
-        name = fresh()
-        body.append(f"  const float v_{name} = {reduce_code(x)};")
-        kind[name] = "scalar"
-        return name
+    def scalar_expr(x) -> str:
+        if isinstance(x, Reduce):
+            return reduce_code(x)
+        if isinstance(x, BinOp):
+            return _BIN[x.op].format(a=scalar_expr(x.a), b=scalar_expr(x.b))
+        if isinstance(x, UnOp):
+            return _UN[x.op].format(a=scalar_expr(x.a))
+        if isinstance(x, Load) and spec.param(x.param).rank == 0:
+            return f"s_{x.param}"
+        if isinstance(x, Local):
+            return f"v_{x.name}"
+        if isinstance(x, ConstF):
+            return fill(x.value)
+        if isinstance(x, ShapeOf):
+            return expr(x)
+        if isinstance(x, Zeros):
+            return "0.0f"
+        raise CodegenError(f"scalar expression {type(x).__name__}")
 
-    stored = set()
-    for st in spec.application:
-        if isinstance(st, ForRange):
-            raise CodegenError("loops (ForRange) are not generated")
-        if isinstance(st, (Let, Assign, Accumulate)):
-            k = ekind(st.expr)
-            if isinstance(st, Let):
-                kind[st.name] = k
-                if k == "elem":
-                    body.append(f"  float v_{st.name}[E];")
-            elif st.name not in kind:
-                raise CodegenError(f"assignment to undefined local {st.name!r}")
-            elif kind[st.name] == "scalar" and k == "elem":
-                raise CodegenError(f"local {st.name!r} changes from tile-scalar to element-wise")
-            x = hoist(st.expr)
-            if isinstance(st, Accumulate):
-                x = BinOp("+", Local(st.name), x)
-            if kind[st.name] == "elem":
-                name = st.name
-                elem_loop(lambda e: body.append(f"    v_{name}[{e}] = {expr(x, e)};"))
+    def statements(stmts, top):
+        for st in stmts:
+            if isinstance(st, ForRange):
+                lv = f"lv_{st.var}"
+                if isinstance(st.extent, ShapeOf) and st.extent.of == "nest":
+                    ext_c = _render(maps[st.extent.param].nest_sizes[st.extent.dim], gsym)
+                elif isinstance(st.extent, (int, IConst)):
+                    ext_c = str(int(getattr(st.extent, "value", st.extent)))
+                else:
+                    ext_c = _render(st.extent, gsym)
+                emit(f"for (i64 {lv} = 0; {lv} < ({ext_c}); ++{lv}) {{")
+                loopvar[st.var] = lv
+                ind[0] += "  "
+                statements(st.body, False)
+                ind[0] = ind[0][:-2]
+                del loopvar[st.var]
+                emit("}")
+            elif isinstance(st, (Let, Assign, Accumulate)):
+                k = ekind(st.expr)
+                if isinstance(st, Let):
+                    if not top:
+                        raise CodegenError("declarations inside loops are not generated")
+                    kind[st.name] = k
+                    if k == "elem":
+                        emit(f"float v_{st.name}[E];")
+                elif st.name not in kind:
+                    raise CodegenError(f"assignment to undefined local {st.name!r}")
+                elif kind[st.name] == "scalar" and k == "elem":
+                    raise CodegenError(f"local {st.name!r} changes from tile-scalar to "
+                                       "element-wise")
+                x = hoist(st.expr)
+                if isinstance(st, Accumulate):
+                    x = BinOp("+", Local(st.name), x)
+                if kind[st.name] == "elem":
+                    name = st.name
+                    elem_loop(lambda: emit(f"  v_{name}[e] = {expr(x)};"))
+                else:
+                    decl = "float " if isinstance(st, Let) else ""
+                    emit(f"{decl}v_{st.name} = {scalar_expr(x)};")
+            elif isinstance(st, Store):
+                if not top:
+                    raise CodegenError("stores inside loops are not generated")
+                ekind(st.expr)
+                x = hoist(st.expr)
+                off, mask = off_mask(st.param, map_sym(st.param, st.nests, elem_lane(st.param)))
+                pi = tnames.index(st.param)
+                elem_loop(lambda: emit(f"  if ({mask}) p{pi}[{off}] = from_f<T>({expr(x)});"))
             else:
-                decl = "float " if isinstance(st, Let) else ""
-                body.append(f"  {decl}v_{st.name} = {scalar_expr(x)};")
-        elif isinstance(st, Store):
-            m = maps[st.param]
-            for n in st.nests:
-                if not isinstance(n, IConst):
-                    raise CodegenError("stores with loop-variable nest indices are not generated")
-            ekind(st.expr)
-            x = hoist(st.expr)
-            nests = {f"nest_{k}": int(n.value) for k, n in enumerate(st.nests)}
-            bcast = ext[st.param]
-            pi = [t.name for t in tensors].index(st.param)
+                raise CodegenError(f"statement {type(st).__name__}")
 
-            def sym(name, nests=nests, bcast=bcast):
-                if name.startswith("lane_"):
-                    j = int(name[5:])
-                    return "((i64)0)" if bcast[j] == 1 and uni[j] != 1 else f"L{j}_e"
-                if name.startswith("nest_"):
-                    return f"((i64){nests.get(name, 0)}LL)"
-                return gsym(name)
-
-            off = _render(m.offset, sym)
-            conds = [f"(({_render(lhs, sym)}) >= 0 && ({_render(lhs, sym)}) < ({_render(b, sym)}))"
-                     for lhs, b in m.mask]
-            mask = " && ".join(conds) if conds else "true"
-
-            def emit_store(e, x=x, off=off, mask=mask, pi=pi):
-                body.append(f"    if ({mask}) p{pi}[{off}] = from_f<T>({expr(x, e)});")
-
-            elem_loop(emit_store)
-            stored.add(st.param)
-        else:
-            raise CodegenError(f"statement {type(st).__name__}")
+    statements(spec.application, True)
 
     # lane coordinates of element e of this thread (row-major in the universe)
     lane_decode = []
     for e in range(per_thread):
         lane_decode.append(f"  const i64 li_{e} = (i64)threadIdx.x + {e * block}LL;")
-        rem = f"li_{e}"
         for j in range(nd):
             inner = math.prod(uni[j + 1:]) if j + 1 < nd else 1
-            lane_decode.append(f"  const i64 L{j}_{e} = ({rem} / {inner}LL) % {uni[j]}LL;")
-    # the body refers to per-element lane variables as L{j}_e with e the loop
-    # index: materialise them through small arrays
-    arrays = []
-    for j in range(nd):
-        arrays.append(f"  i64 Larr{j}[E] = {{{', '.join(f'L{j}_{e}' for e in range(per_thread))}}};")
-    text_body = "\n".join(body)
-    for j in range(nd):
-        text_body = text_body.replace(f"L{j}_e", f"Larr{j}[e]")
+            lane_decode.append(f"  const i64 L{j}_{e} = (li_{e} / {inner}LL) % {uni[j]}LL;")
+    arrays = [f"  const i64 Larr{j}[E] = {{{', '.join(f'L{j}_{e}' for e in range(per_thread))}}};"
+              for j in range(nd)]
 
     ctype = _CT[dtype]
     args = [f"T* __restrict__ p{i}" for i in range(len(tensors))]
@@ -408,21 +512,19 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
         f"extern \"C\" __global__ void __launch_bounds__(NT) ntb_generated({', '.join(args)}) {{",
         "  __shared__ float red[NT / 32];",
         "  (void)red;",
+        *shared_decls,
         "  const i64 pid = (i64)blockIdx.x;",
         *pid_lines,
         *lane_decode,
         *arrays,
         "  bool V[E];",
         *[f"  V[{e}] = li_{e} < LANES;" for e in range(per_thread)],
-        text_body,
+        *body,
         "}",
     ])
-    if not stored:
-        raise CodegenError("the application stores nothing")
-    name = "ntb_generated"
-    return Generated(source=src, name=name, slot_names=tuple(slot_names),
-                     tensor_params=tuple(p.name for p in tensors),
-                     scalar_params=tuple(p.name for p in scalars), block=block)
+    return Generated(source=src, name="ntb_generated", slot_names=tuple(slot_names),
+                     tensor_params=tuple(tnames), scalar_params=tuple(p.name for p in scalars),
+                     block=block)
 
 
 def source_digest(g: Generated) -> str:

@@ -19,7 +19,8 @@ application, tensors)`` (PAPER.md:307-324, 341-348, 550-580).
   IR (spec.py).  Supported: assignment (a parameter assigned to is an
   output -> Store), ``+=`` (Accumulate), ``for k in range(t.shape[i])``,
   ``t[k]`` nest loads, ``+ - * /``, numbers, ``t.shape[i]`` and the ``ntl``
-  calls ``zeros, dot, exp, sqrt, sigmoid, max, sum``.
+  calls ``zeros, dot, exp, sqrt, sigmoid, log, rsqrt, abs, tanh, relu, max,
+  sum`` and the elementwise ``maximum, minimum``.
 * The result is typechecked into a CheckedSpec and executed by
   ``backend.launch``, which matches it STRUCTURALLY (names of locals,
   parameters and the kernel itself do not matter) to one of the native
@@ -70,6 +71,7 @@ class _Lang:
         raise RuntimeError("ntl calls are compiled, not executed")
 
     dot = exp = sqrt = sigmoid = max = sum = zeros
+    log = rsqrt = abs = tanh = relu = maximum = minimum = zeros
 
 
 language = _Lang()
@@ -234,8 +236,11 @@ class _Compiler(ast.NodeVisitor):
                 return Zeros(self.shape_arg(n.args[0]), "f32")
             if fn == "dot":
                 return Dot(self.expr(n.args[0]), self.expr(n.args[1]))
-            if fn in ("exp", "sqrt", "sigmoid"):
+            if fn in ("exp", "sqrt", "sigmoid", "log", "rsqrt", "abs", "tanh", "relu"):
                 return UnOp(fn, self.expr(n.args[0]))
+            if fn in ("maximum", "minimum"):
+                return BinOp("max" if fn == "maximum" else "min", self.expr(n.args[0]),
+                             self.expr(n.args[1]))
             if fn in ("max", "sum"):
                 arg = self.expr(n.args[0])
                 kw = [k.value for k in n.keywords if k.arg == "axis"]

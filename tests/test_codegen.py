@@ -54,6 +54,31 @@ def l2norm_kernel():
     return make(arrangement, application, (Tensor(2), Tensor(2)))
 
 
+BM = Symbol("BM", constexpr=True)
+BN = Symbol("BN", constexpr=True)
+BK = Symbol("BK", constexpr=True)
+
+
+def mm_relu_kernel():
+    """The paper's matmul arrangement with a fused ReLU epilogue: a
+    contraction no native family implements."""
+    def arrangement(input, other, output, BM=BM, BN=BN, BK=BK):
+        output_tiled = output.tile((BM, BN))
+        input_tiled = input.tile((BM, BK)).tile((1, -1)).expand((-1, output_tiled.shape[1]))
+        input_tiled.dtype = input_tiled.dtype.squeeze(0)
+        other_tiled = other.tile((BK, BN)).tile((-1, 1)).expand((output_tiled.shape[0], -1))
+        other_tiled.dtype = other_tiled.dtype.squeeze(1)
+        return input_tiled, other_tiled, output_tiled
+
+    def application(input, other, output):
+        accumulator = ntl.zeros(output.shape, dtype=ntl.float32)
+        for k in range(input.shape[0]):
+            accumulator += ntl.dot(input[k], other[k])
+        output = ntl.maximum(accumulator, 0.0)  # noqa: F841
+
+    return make(arrangement, application, (Tensor(2), Tensor(2), Tensor(2)))
+
+
 def _binding(k, shapes, meta):
     b = dict(meta)
     for p, shp in zip(k.checked.spec.params, shapes):
@@ -72,6 +97,7 @@ CASES = [
     (gelu_kernel, [(777,)] * 2, {"BLOCK": 256}),
     (temp_softmax_kernel, [(33, 1000)] * 2, {"BLOCK": 1024}),
     (l2norm_kernel, [(7, 4096)] * 2, {"BLOCK": 4096}),
+    (mm_relu_kernel, [(200, 96), (96, 130), (200, 130)], {"BM": 32, "BN": 32, "BK": 32}),
 ]
 
 
@@ -146,3 +172,22 @@ def test_generic_row_reductions_on_b200():
     (xin,), out = _run(l2norm_kernel(), [x], {"BLOCK": 4096}, torch.float16)
     ref = xin / np.sqrt((xin.astype(np.float64) ** 2).sum(1, keepdims=True) + 1e-6)
     np.testing.assert_allclose(out, ref, rtol=1e-2, atol=1e-3)
+
+
+@pytest.mark.gpu
+def test_generic_contraction_on_b200():
+    import torch
+
+    rng = np.random.default_rng(3)
+    a = rng.uniform(-1, 1, (200, 96)).astype(np.float32)
+    b = rng.uniform(-1, 1, (96, 130)).astype(np.float32)
+    for dt in (torch.float32, torch.float16):
+        ta, tb = torch.from_numpy(a).cuda().to(dt), torch.from_numpy(b).cuda().to(dt)
+        out = torch.empty((200, 130), device="cuda", dtype=dt)
+        before = backend.path_counts()["jit"]
+        mm_relu_kernel()(ta, tb, out, BM=32, BN=32, BK=32)
+        torch.cuda.synchronize()
+        assert backend.path_counts()["jit"] == before + 1
+        ref = np.maximum(ta.float().cpu().numpy() @ tb.float().cpu().numpy(), 0)
+        tol = 1e-4 if dt == torch.float32 else 1e-2
+        np.testing.assert_allclose(out.float().cpu().numpy(), ref, rtol=tol, atol=tol)
