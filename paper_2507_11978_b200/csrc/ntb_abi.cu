@@ -283,7 +283,11 @@ int ntb_launch(int kernel, int dtype, void* const* ptrs, int n_ptrs, const doubl
     if (ranks[i] < 1 || ranks[i] > 4) return fail(NTB_ERR_ARG, "tensor rank out of range");
     a.base[i] = off;
     off += ranks[i];
-    if (!ptrs[i]) return fail(NTB_ERR_ARG, "null tensor pointer");
+    int64_t numel = 1;
+    for (int d = 0; d < ranks[i]; ++d) numel *= sizes[a.base[i] + d];
+    // an empty tensor (e.g. the K = 0 operands of a zero-length contraction)
+    // may have a null data pointer; nothing is read from it
+    if (!ptrs[i] && numel > 0) return fail(NTB_ERR_ARG, "null tensor pointer");
   }
   switch (kernel) {
     case NTB_K_ADD:

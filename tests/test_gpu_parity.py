@@ -426,3 +426,55 @@ def test_cpu_tensors_are_rejected():
     a = torch.ones(8)
     with pytest.raises(backend.LaunchError, match="CUDA tensor"):
         backend.add_launch(a, a, torch.empty(8), 4)
+
+
+@pytest.mark.parametrize("case", ["add", "silu", "softmax", "rms_norm", "mm_m0", "bmm_b0",
+                                  "conv_n0", "sdpa_b0", "rope_s0"])
+def test_empty_grid_is_a_launch_error_like_the_reference(case):
+    """An empty grid raises LaunchError("grid dimension evaluated to 0"),
+    exactly as sim.launch does (sim.py:180-182)."""
+    f16 = torch.float16
+    z = lambda *s, dt=f16: torch.zeros(s, device=DEV, dtype=dt)  # noqa: E731
+    calls = {
+        "add": lambda: backend.add_launch(z(0, dt=torch.float32), z(0, dt=torch.float32),
+                                          z(0, dt=torch.float32), 1024),
+        "silu": lambda: backend.silu_launch(z(0), z(0), 1024),
+        "softmax": lambda: backend.softmax_launch(z(0, 64), z(0, 64), 64),
+        "rms_norm": lambda: backend.rms_norm_launch(z(0, 64), z(64), z(0, 64), 64),
+        "mm_m0": lambda: backend.mm_launch(z(0, 64), z(64, 32), z(0, 32), 64, 64, 32),
+        "bmm_b0": lambda: backend.bmm_launch(z(0, 64, 64), z(0, 64, 64), z(0, 64, 64), 64, 64, 32),
+        "conv_n0": lambda: backend.conv2d_launch(z(0, 8, 10, 10), z(16, 8, 3, 3), z(0, 16, 8, 8),
+                                                 64, 64, 32),
+        "sdpa_b0": lambda: backend.sdpa_launch(z(0, 2, 64, 64), z(0, 2, 64, 64), z(0, 2, 64, 64),
+                                               z(0, 2, 64, 64), 128, 128),
+        "rope_s0": lambda: backend.rope_launch(z(2, 0, 4, 64), z(0, 32), z(0, 32), z(2, 0, 4, 64),
+                                               32),
+    }
+    with pytest.raises(backend.LaunchError, match="grid dimension evaluated to 0"):
+        calls[case]()
+
+
+@pytest.mark.parametrize("kernel", ["mm", "addmm", "bmm"])
+def test_zero_length_contraction_stores_the_epilogue(kernel):
+    """K = 0: the reference's K loop runs zero times, so mm stores zeros and
+    addmm stores beta * input (sim.py:269-363)."""
+    f16 = torch.float16
+    meta = (64, 64, 32)
+    if kernel == "bmm":
+        out = torch.full((2, 48, 40), 7.0, device=DEV, dtype=f16)
+        backend.bmm_launch(torch.zeros((2, 48, 0), device=DEV, dtype=f16),
+                           torch.zeros((2, 0, 40), device=DEV, dtype=f16), out, *meta)
+        ref = torch.zeros_like(out)
+    elif kernel == "mm":
+        out = torch.full((48, 40), 7.0, device=DEV, dtype=f16)
+        backend.mm_launch(torch.zeros((48, 0), device=DEV, dtype=f16),
+                          torch.zeros((0, 40), device=DEV, dtype=f16), out, *meta)
+        ref = torch.zeros_like(out)
+    else:
+        inp = torch.randn((48, 40), device=DEV).to(f16)
+        out = torch.full((48, 40), 7.0, device=DEV, dtype=f16)
+        backend.addmm_launch(inp, torch.zeros((48, 0), device=DEV, dtype=f16),
+                             torch.zeros((0, 40), device=DEV, dtype=f16), 0.5, -2.0, out, *meta)
+        ref = (inp.float() * 0.5).to(f16)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
