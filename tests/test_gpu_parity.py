@@ -478,3 +478,20 @@ def test_zero_length_contraction_stores_the_epilogue(kernel):
         ref = (inp.float() * 0.5).to(f16)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_add_beyond_int32_elements():
+    """2^31 + 4104 elements (past the reference's int32 Triton offsets,
+    SURVEY 8(a) A7): the kernels index in int64; checked at the far end."""
+    n = (1 << 31) + 4104
+    a = torch.ones(n, device=DEV, dtype=torch.float16)
+    b = torch.empty(n, device=DEV, dtype=torch.float16)
+    b[-8192:] = torch.arange(8192, device=DEV, dtype=torch.float16) * 0.25
+    b[:-8192] = 0.5
+    out = torch.empty_like(a)
+    backend.add_launch(a, b, out, 1024)
+    torch.cuda.synchronize()
+    assert torch.equal(out[-8192:], (a[-8192:].float() + b[-8192:].float()).half())
+    assert float(out[: 1 << 20].float().mean()) == 1.5
+    del a, b, out
+    torch.cuda.empty_cache()
