@@ -90,3 +90,33 @@ def test_builder_sdpa_rope_restatements():
     # rotation preserves the norm of each (x_i, x_{i+half}) pair
     np.testing.assert_allclose(np.sum(y.astype(np.float64) ** 2, -1), np.sum(x ** 2, -1),
                                rtol=1e-5)
+
+
+def test_builder_oracles_against_torch():
+    """The builder-written sdpa / rope / sdpa_rope oracles against independent
+    torch implementations (f64 on the CPU): torch's scaled_dot_product_attention
+    and a complex-number rotary embedding (rotation of (x_i + j x_{i+D/2}) by
+    the angle whose cos / sin are the tables)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(1)
+    q, k, v = (rng.standard_normal((2, 3, 37, 16)) for _ in range(3))
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(q), torch.from_numpy(k), torch.from_numpy(v)).numpy()
+    np.testing.assert_allclose(oracle.sdpa(q, k, v), ref, rtol=1e-5, atol=1e-6)
+    ang = rng.uniform(-3, 3, (37, 8))
+    sin, cos = np.sin(ang), np.cos(ang)
+
+    def rope_complex(x_bshd):
+        z = torch.complex(torch.from_numpy(x_bshd[..., :8]), torch.from_numpy(x_bshd[..., 8:]))
+        z = z * torch.polar(torch.ones(37, 8, dtype=torch.float64),
+                            torch.from_numpy(ang))[None, :, None, :]
+        return torch.cat([z.real, z.imag], -1).numpy()
+
+    x = rng.standard_normal((2, 37, 3, 16))
+    np.testing.assert_allclose(oracle.rope(x, sin, cos), rope_complex(x), rtol=1e-5, atol=1e-6)
+    qb, kb = np.swapaxes(rope_complex(np.swapaxes(q, 1, 2)), 1, 2), \
+        np.swapaxes(rope_complex(np.swapaxes(k, 1, 2)), 1, 2)
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        torch.from_numpy(qb), torch.from_numpy(kb), torch.from_numpy(v)).numpy()
+    np.testing.assert_allclose(oracle.sdpa_rope(q, k, v, sin, cos, sin, cos), ref,
+                               rtol=1e-5, atol=1e-6)
