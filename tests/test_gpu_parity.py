@@ -495,3 +495,20 @@ def test_add_beyond_int32_elements():
     assert float(out[: 1 << 20].float().mean()) == 1.5
     del a, b, out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("sq,sk", [(300, 700), (1000, 64), (129, 1)])
+def test_sdpa_cross_attention_lengths(sq, sk):
+    """S_q != S_k (cross attention): partial query tiles, partial and single-key
+    KV tiles, more KV tiles than query tiles and the reverse."""
+    rng = np.random.default_rng(sq * 7 + sk)
+    b, h, d = 2, 5, 128
+    q = _r16(rng.uniform(-1, 1, (b, h, sq, d)).astype(np.float32), torch.float16)
+    k = _r16(rng.uniform(-1, 1, (b, h, sk, d)).astype(np.float32), torch.float16)
+    v = _r16(rng.uniform(-1, 1, (b, h, sk, d)).astype(np.float32), torch.float16)
+    with _Paths() as pc:
+        got = _run("sdpa", {"q": q, "k": k, "v": v, "o": None},
+                   {"BLOCK_SIZE_M": 128, "BLOCK_SIZE_N": 128}, torch.float16,
+                   out=torch.zeros((b, h, sq, d), device=DEV, dtype=torch.float16))
+    assert pc.delta["attn_tc"] == 1
+    _close(got, oracle.sdpa(q, k, v), rtol=1e-2, atol=1e-2)
