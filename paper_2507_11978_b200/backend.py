@@ -30,7 +30,7 @@ from __future__ import annotations
 import ctypes
 import threading
 from dataclasses import dataclass
-from typing import Mapping
+from typing import Mapping, Optional
 
 import numpy as np
 
@@ -57,6 +57,9 @@ class BackendError(RuntimeError):
 class LaunchResult:
     grid: tuple
     total: int
+    # collect_writes=True: per out-parameter, per program (forward pid order),
+    # the sorted flat offsets the program writes (sim.LaunchResult.writes)
+    writes: Optional[dict] = None
 
 
 _DTYPES = None
@@ -315,7 +318,53 @@ def _plan_key(checked, args: Mapping, meta: Mapping):
     return tuple(parts)
 
 
-def launch(checked, args: Mapping, meta: Mapping, *, stream=None) -> LaunchResult:
+def program_writes(checked, args: Mapping, meta: Mapping) -> dict:
+    """Per out-parameter, per program, the sorted flat offsets it writes -
+    enumerated by the native map VM on the host (ntb_map_enumerate) from the
+    same lowered maps the kernels use; the reference collects the same sets
+    while simulating (sim.py:288-290, 348)."""
+    spec = checked.spec
+    binding = _binding(spec, args, meta)
+    _, prog = _resolve(checked, allow_generic=True)
+    grid = evaluate_grid(checked, binding)
+    total = int(np.prod(grid))
+    slots = prog.slots(binding)
+    out = {}
+    for p in spec.params:
+        if p.role != "out":
+            continue
+        rc, offs, mask = _lib.map_enumerate(prog.blob, prog.params.index(p.name), slots)
+        if rc:
+            raise BackendError(_lib.last_error())
+        per = len(offs) // total
+        m = mask.astype(bool)
+        out[p.name] = [np.sort(offs[i * per:(i + 1) * per][m[i * per:(i + 1) * per]])
+                       for i in range(total)]
+    return out
+
+
+def check_write_partition(checked, args: Mapping, meta: Mapping) -> None:
+    """sim.check_write_partition twin (sim.py:366-393): per out-parameter the
+    programs' writes are pairwise disjoint and cover every element of the
+    argument exactly once."""
+    writes = program_writes(checked, args, meta)
+    for name, per_program in writes.items():
+        allo = np.concatenate(per_program) if per_program else np.empty(0, dtype=np.int64)
+        if len(np.unique(allo)) != allo.size:
+            raise BackendError(f"programs overlap when writing {name!r}(size {allo.size})")
+        t = args[name]
+        idx = np.zeros(tuple(t.shape), dtype=np.int64)
+        for d, (n, st) in enumerate(zip(t.shape, t.stride())):
+            shape = [1] * len(t.shape)
+            shape[d] = n
+            idx = idx + (np.arange(n, dtype=np.int64) * st).reshape(shape)
+        if not np.array_equal(np.sort(allo), np.sort(idx.ravel())):
+            raise BackendError(f"writes to {name!r} do not cover it exactly: wrote {allo.size} "
+                               f"of {idx.size} elements")
+
+
+def launch(checked, args: Mapping, meta: Mapping, *, stream=None, pid_order: str = "forward",
+           collect_writes: bool = False) -> LaunchResult:
     """Execute a CheckedSpec on the current CUDA device (sim.launch twin).
 
     The first call for a given (spec, shapes, strides, dtype, meta, scalars)
@@ -325,6 +374,10 @@ def launch(checked, args: Mapping, meta: Mapping, *, stream=None) -> LaunchResul
     """
     import torch
 
+    # programs write disjoint outputs (check_write_partition), so their order
+    # on the GPU cannot change the result; the reference's knob is accepted
+    if pid_order not in ("forward", "reverse"):
+        raise LaunchError(f"unknown pid order {pid_order!r}")
     key = _plan_key(checked, args, meta)
     plan = _plans.get(key)
     if plan is None or plan[0] is not checked:
@@ -333,7 +386,9 @@ def launch(checked, args: Mapping, meta: Mapping, *, stream=None) -> LaunchResul
             _plans.clear()
         _plans[key] = plan
     if plan[1] == "jit":
-        return _launch_generated(plan, args, stream)
+        res = _launch_generated(plan, args, stream)
+        return LaunchResult(res.grid, res.total, program_writes(checked, args, meta)) \
+            if collect_writes else res
     _, names, kid, dt, n, sizes, strides, ranks, metas, sc, n_sc, result, dev = plan
     ptrs = (ctypes.c_void_p * n)(*[args[nm].data_ptr() for nm in names])
     if stream is None:
@@ -347,6 +402,8 @@ def launch(checked, args: Mapping, meta: Mapping, *, stream=None) -> LaunchResul
         raise LaunchError(_lib.last_error())
     if rc:
         raise BackendError(_lib.last_error())
+    if collect_writes:
+        return LaunchResult(result.grid, result.total, program_writes(checked, args, meta))
     return result
 
 

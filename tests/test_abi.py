@@ -153,3 +153,27 @@ def test_sdpa_rope_is_its_own_family():
     assert _lib.KERNEL_IDS["sdpa_rope"] == 11
     hdr = Path(__file__).resolve().parent.parent / "include" / "ntb200.h"
     assert "NTB_K_SDPA_ROPE = 11" in hdr.read_text()
+
+
+@pytest.mark.parametrize("kernel,shapes,meta", [
+    ("add", {"input": (1000,), "other": (1000,), "output": (1000,)}, {"BLOCK_SIZE": 64}),
+    ("softmax", {"input": (5, 20), "output": (5, 20)}, {"COLS_PADDED": 32}),
+    ("mm", {"input": (70, 40), "other": (40, 90), "output": (70, 90)},
+     {"BLOCK_SIZE_M": 32, "BLOCK_SIZE_N": 16, "BLOCK_SIZE_K": 8}),
+    ("bmm", {"input": (3, 20, 24), "other": (3, 24, 18), "output": (3, 20, 18)},
+     {"BLOCK_SIZE_M": 8, "BLOCK_SIZE_N": 16, "BLOCK_SIZE_K": 8}),
+    ("conv2d", {"input": (2, 3, 9, 7), "filter": (4, 3, 3, 2), "output": (2, 4, 7, 6)},
+     {"BLOCK_SIZE_M": 16, "BLOCK_SIZE_N": 4, "BLOCK_SIZE_K": 8}),
+    ("rope", {"input": (2, 5, 3, 8), "sin": (5, 4), "cos": (5, 4), "output": (2, 5, 3, 8)},
+     {"HALF_D": 4}),
+])
+def test_write_partition_matches_the_reference_contract(kernel, shapes, meta):
+    """sim.check_write_partition twin on the native map VM: every catalog
+    kernel's programs write disjoint sets covering each output exactly once
+    (sim.py:366-393), and launch(..., collect_writes=True) reports them."""
+    ck = C.checked(kernel)
+    args = {n: _Fake(s) for n, s in shapes.items()}
+    backend.check_write_partition(ck, args, meta)
+    w = backend.program_writes(ck, args, meta)
+    out = [p.name for p in ck.spec.params if p.role == "out"][0]
+    assert sum(len(x) for x in w[out]) == int(np.prod(shapes[out]))

@@ -512,3 +512,23 @@ def test_sdpa_cross_attention_lengths(sq, sk):
                    out=torch.zeros((b, h, sq, d), device=DEV, dtype=torch.float16))
     assert pc.delta["attn_tc"] == 1
     _close(got, oracle.sdpa(q, k, v), rtol=1e-2, atol=1e-2)
+
+
+def test_launch_accepts_the_simulator_knobs():
+    """launch(..., pid_order="reverse", collect_writes=True) like sim.launch:
+    same output for either order, writes reported per program."""
+    rng = np.random.default_rng(9)
+    a = _t(rng.uniform(-1, 1, 3000).astype(np.float32))
+    b = _t(rng.uniform(-1, 1, 3000).astype(np.float32))
+    outs = []
+    for order in ("forward", "reverse"):
+        out = torch.zeros(3000, device=DEV)
+        res = backend.launch(C.checked("add"), {"input": a, "other": b, "output": out},
+                             {"BLOCK_SIZE": 1024}, pid_order=order, collect_writes=True)
+        torch.cuda.synchronize()
+        outs.append(out.cpu())
+        assert res.total == 3 and [len(w) for w in res.writes["output"]] == [1024, 1024, 952]
+    assert torch.equal(outs[0], outs[1])
+    with pytest.raises(backend.LaunchError, match="unknown pid order"):
+        backend.launch(C.checked("add"), {"input": a, "other": b, "output": out},
+                       {"BLOCK_SIZE": 1024}, pid_order="random")
