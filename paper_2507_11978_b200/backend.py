@@ -508,6 +508,31 @@ def _make_plan(checked, args: Mapping, meta: Mapping):
             metas, sc, len(scalars), LaunchResult(grid=tuple(grid), total=total), ts[0].device)
 
 
+def simulate(kernel: str, args: Mapping, meta: Mapping, pid_order: str = "forward",
+             dtype=None) -> np.ndarray:
+    """GPU twin of the reference's ``verify.simulate`` (verify.py:200-204):
+    ``args`` maps every parameter of the catalog kernel to a host numpy
+    array (outputs included, as ``verify.make_inputs`` builds them) or a float
+    (rank-0 parameters); the arrays go to the current CUDA device as
+    ``dtype`` (default float32, the catalog's f32 kind), the kernel runs on
+    its native sm_100a path, and the output comes back as numpy."""
+    import torch
+
+    dtype = torch.float32 if dtype is None else dtype
+    ck = canonical(kernel)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    targs = {}
+    for p in ck.spec.params:
+        if p.name not in args:
+            raise LaunchError(f"missing argument {p.name!r}")
+        v = args[p.name]
+        targs[p.name] = float(v) if p.rank == 0 else \
+            torch.from_numpy(np.ascontiguousarray(v)).to(dev, dtype)
+    launch(ck, targs, meta, pid_order=pid_order)
+    outs = [p.name for p in ck.spec.params if p.role == "out"]
+    return targs[outs[0]].float().cpu().numpy()
+
+
 def launch_count() -> int:
     """Kernels launched by libntb200 in this process."""
     return int(_lib.lib().ntb_launch_count())

@@ -532,3 +532,23 @@ def test_launch_accepts_the_simulator_knobs():
     with pytest.raises(backend.LaunchError, match="unknown pid order"):
         backend.launch(C.checked("add"), {"input": a, "other": b, "output": out},
                        {"BLOCK_SIZE": 1024}, pid_order="random")
+
+
+@pytest.mark.parametrize("kernel", ["add", "softmax", "mm", "conv2d"])
+def test_verify_simulate_twin(kernel):
+    """backend.simulate(kernel, args, meta) == the reference's
+    verify.simulate outputs committed in tests/golden (same inputs)."""
+    index, arrays = sim_cases()
+    done = 0
+    for ci, case in enumerate(index):
+        if case["kernel"] != kernel or done >= 3:
+            continue
+        args = case_args(ci, case, arrays)
+        outs = [p.name for p in C.checked(kernel).spec.params if p.role == "out"]
+        args[outs[0]] = np.zeros(out_shape(kernel, args), dtype=np.float32)
+        got = backend.simulate(kernel, args, case["meta"], pid_order="reverse")
+        sim = arrays[f"c{ci}_sim"]
+        tol = 0.0 if kernel == "add" else 1e-4
+        assert float(np.max(np.abs(got.astype(np.float64) - sim), initial=0.0)) <= tol
+        done += 1
+    assert done == 3
