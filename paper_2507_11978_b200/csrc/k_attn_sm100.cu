@@ -49,8 +49,14 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define NTB_ATTN_STAGED 1  // measured 7.18 vs 7.27 ms (B32 H32 S4096 D128)
 #endif
 #ifndef NTB_ATTN_POLY_PAIRS
-#define NTB_ATTN_POLY_PAIRS 3  // of every 16 score pairs, 2^x on the FMA pipe
+#define NTB_ATTN_POLY_PAIRS 4  // of every 16 score pairs, 2^x on the FMA pipe
 #endif
+
+#ifndef NTB_ATTN_PCH
+#define NTB_ATTN_PCH 4  // P_j released to the MMA warp in this many key chunks (4: ~2% over 2)
+#endif
+constexpr int PCH = NTB_ATTN_PCH;
+static_assert(PCH == 2 || PCH == 4, "P chunks");
 
 #ifndef NTB_ATTN_TRACE
 #define NTB_ATTN_TRACE 0  // debug builds: per-phase clock64 stamps of CTA 0's first item
@@ -155,15 +161,23 @@ __device__ __forceinline__ void rope_tile(uint8_t* tile, int chunk_bytes, int ro
   }
 }
 
+#ifndef NTB_ATTN_QDB
+#define NTB_ATTN_QDB 0  // double-buffer Q in plain sdpa too (always with rope)
+#endif
+
 template <int D, bool ROPE = false>
 struct Layout {
   static constexpr int DCH = D / 64;               // 128B chunks along D
   static constexpr int Q_BYTES = BM * D * 2;       // one query tile
   static constexpr int CH = BN * 128;              // one 64-wide chunk of a K/V tile
   static constexpr int SLOT = DCH * CH;            // one K or V tile
-  static constexpr int NS = D == 128 ? 5 : 8;      // K/V ring entries
+  // Q buffers: with rope the next item's two query tiles are loaded and
+  // rotated while the current item runs (the rotation is L2-latency bound,
+  // ~5 us per item, and would otherwise stall the tensor core between items)
+  static constexpr int QB = (ROPE || NTB_ATTN_QDB) ? 2 : 1;
+  static constexpr int NS = D == 128 ? (QB == 2 ? 3 : 5) : 8;  // K/V ring entries
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_KV = 2 * Q_BYTES;
+  static constexpr int OFF_KV = QB * 2 * Q_BYTES;
   static constexpr int SMEM = OFF_KV + NS * SLOT + 1024;
   static constexpr uint32_t T_S0 = 0, T_S1 = BN, T_O0 = 2 * BN, T_O1 = 2 * BN + D;
   static_assert(2 * BN + 2 * D <= 512, "TMEM budget");
@@ -209,28 +223,29 @@ __global__ void __launch_bounds__(384, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t q_full, q_empty, kv_full[L::NS], kv_empty[L::NS], s_full[2],
-      p_full[2][2], o_full[2], o_empty[2], q_rot;
+  __shared__ __align__(8) uint64_t q_full[L::QB], q_empty[L::QB], kv_full[L::NS], kv_empty[L::NS],
+      s_full[2], p_full[2][PCH], o_full[2], o_empty[2], q_rot[L::QB];
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_kv = (p.Sk + BN - 1) / BN;
 
   if (threadIdx.x == 0) {
-    mbar_init(&q_full, 1);
-    mbar_init(&q_empty, 1);
+    for (int i = 0; i < L::QB; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&q_rot[i], 2);                  // rope warps 2-3
+    }
     for (int i = 0; i < L::NS; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&s_full[g], 1);
-      mbar_init(&p_full[g][0], 4);
-      mbar_init(&p_full[g][1], 4);
+      for (int q = 0; q < PCH; ++q) mbar_init(&p_full[g][q], 4);
       mbar_init(&o_full[g], 1);
       mbar_init(&o_empty[g], 4);
     }
-    mbar_init(&q_rot, 2);                       // rope warps 2-3
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -250,17 +265,25 @@ __global__ void __launch_bounds__(384, 1)
       tma_prefetch(&maps.k);
       tma_prefetch(&maps.v);
       uint32_t c = 0;  // K/V ring sequence number: K_j, V_j, K_{j+1}, ...
-      int it = 0;
-      for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+      auto load_q = [&](int item, int it) {
         const int qt = item % p.n_qt, bh = item / p.n_qt, h = bh % p.H, b = bh / p.H;
-        mbar_wait(&q_empty, (it & 1) ^ 1);
-        mbar_expect_tx(&q_full, 2 * L::Q_BYTES);
+        const int qb = it % L::QB;
+        mbar_wait(&q_empty[qb], ((it / L::QB) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qb], 2 * L::Q_BYTES);
 #pragma unroll
         for (int g = 0; g < 2; ++g)
 #pragma unroll
           for (int ch = 0; ch < L::DCH; ++ch)
-            tma_load_4d(smem + L::OFF_Q + g * L::Q_BYTES + ch * (BM * 128), &maps.q, &q_full,
-                        ch * 64, qt * 2 * BM + g * BM, h, b);
+            tma_load_4d(smem + L::OFF_Q + (qb * 2 + g) * L::Q_BYTES + ch * (BM * 128), &maps.q,
+                        &q_full[qb], ch * 64, qt * 2 * BM + g * BM, h, b);
+      };
+      // two Q buffers: the next item's Q is requested before this item's K/V
+      if (L::QB == 2 && (int)blockIdx.x < p.n_items) load_q(blockIdx.x, 0);
+      int it = 0;
+      for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+        const int bh = item / p.n_qt, h = bh % p.H, b = bh / p.H;
+        if (L::QB == 1) load_q(item, it);
+        else if (item + (int)gridDim.x < p.n_items) load_q(item + gridDim.x, it + 1);
         for (int j = 0; j < n_kv; ++j) {
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv, ++c) {
@@ -290,8 +313,9 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&kv_full[seq % L::NS], (seq / L::NS) & 1);
         tc_fence_after();
       };
+      int qb = 0;  // Q buffer of the current item
       auto issue_s = [&](int g, uint32_t kseq) {
-        const uint32_t q_addr = smem_u32(smem + L::OFF_Q + g * L::Q_BYTES);
+        const uint32_t q_addr = smem_u32(smem + L::OFF_Q + (qb * 2 + g) * L::Q_BYTES);
         const uint32_t k_addr = slot_addr(kseq);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -302,25 +326,26 @@ __global__ void __launch_bounds__(384, 1)
         }
         mma_commit(&s_full[g]);
       };
-      // P.V for one half of the keys (P is released by the softmax in halves)
+      // P.V for one chunk of the keys (P is released by the softmax in PCH chunks)
       auto issue_pv = [&](int g, uint32_t vseq, bool first, int half) {
         const uint32_t v_addr = slot_addr(vseq);
 #pragma unroll
-        for (int k2 = 0; k2 < BN / 32; ++k2) {
-          const int kk = half * (BN / 32) + k2;
+        for (int k2 = 0; k2 < BN / 16 / PCH; ++k2) {
+          const int kk = half * (BN / 16 / PCH) + k2;
           mma_f16_ts(tmem + (g ? L::T_O1 : L::T_O0), tmem + (g ? L::T_S1 : L::T_S0) + kk * 8,
                      umma_desc_sw128(v_addr + kk * 2048, L::CH, 1024), idesc_o,
                      !(first && kk == 0));
         }
       };
       for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
-        mbar_wait(ROPE ? &q_rot : &q_full, it & 1);
+        qb = it % L::QB;
+        mbar_wait(ROPE ? &q_rot[qb] : &q_full[qb], (it / L::QB) & 1);
         tc_fence_after();
         wait_kv(c);
         issue_s(0, c);
         issue_s(1, c);
         mma_commit(&kv_empty[c % L::NS]);
-        if (n_kv == 1) mma_commit(&q_empty);
+        if (n_kv == 1) mma_commit(&q_empty[qb]);
         for (int j = 0; j < n_kv; ++j, ++t) {
           const bool more = j + 1 < n_kv;
           const uint32_t kseq = c + 2 * j, vseq = kseq + 1, knext = kseq + 2;
@@ -335,10 +360,13 @@ __global__ void __launch_bounds__(384, 1)
           }
           wait_kv(vseq);
           issue_pv(0, vseq, j == 0, 0);
-          mbar_wait(&p_full[0][1], t & 1);
-          tc_fence_after();
+#pragma unroll
+          for (int q = 1; q < PCH; ++q) {
+            mbar_wait(&p_full[0][q], t & 1);
+            tc_fence_after();
+            issue_pv(0, vseq, j == 0, q);
+          }
           TRACE_MMA(j, 2)
-          issue_pv(0, vseq, j == 0, 1);
           if (more) {
             wait_kv(knext);
             TRACE_MMA(j, 3)
@@ -356,14 +384,17 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_after();
           }
           issue_pv(1, vseq, j == 0, 0);
-          mbar_wait(&p_full[1][1], t & 1);
-          tc_fence_after();
-          issue_pv(1, vseq, j == 0, 1);
+#pragma unroll
+          for (int q = 1; q < PCH; ++q) {
+            mbar_wait(&p_full[1][q], t & 1);
+            tc_fence_after();
+            issue_pv(1, vseq, j == 0, q);
+          }
           mma_commit(&kv_empty[vseq % L::NS]);
           if (more) {
             issue_s(1, knext);
             mma_commit(&kv_empty[knext % L::NS]);
-            if (j + 2 == n_kv) mma_commit(&q_empty);
+            if (j + 2 == n_kv) mma_commit(&q_empty[qb]);
           } else {
             mma_commit(&o_full[1]);
           }
@@ -381,15 +412,15 @@ __global__ void __launch_bounds__(384, 1)
     const int t = (warp - 2) * 32 + lane;
     int it = 0;
     for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
-      const int qt = item % p.n_qt;
-      mbar_wait(&q_full, it & 1);
+      const int qt = item % p.n_qt, qb = it % L::QB;
+      mbar_wait(&q_full[qb], (it / L::QB) & 1);
 #pragma unroll 1
       for (int g = 0; g < 2; ++g)
-        rope_tile<D, BF16>(smem + L::OFF_Q + g * L::Q_BYTES, BM * 128, BM,
+        rope_tile<D, BF16>(smem + L::OFF_Q + (qb * 2 + g) * L::Q_BYTES, BM * 128, BM,
                            qt * 2 * BM + g * BM, p.Sq, p.sin_q, p.sq_rs, p.cos_q, p.cq_rs, t, 64);
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&q_rot);
+      if (lane == 0) mbar_arrive(&q_rot[qb]);
     }
   }
   } else {
@@ -456,10 +487,10 @@ __global__ void __launch_bounds__(384, 1)
         const float2 nm2 = make_float2(-m_new, -m_new);
         float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int half = 0; half < PCH; ++half) {
 #pragma unroll
-          for (int c2 = 0; c2 < BN / 64; ++c2) {
-            const int ch = half * (BN / 64) + c2;
+          for (int c2 = 0; c2 < BN / 32 / PCH; ++c2) {
+            const int ch = half * (BN / 32 / PCH) + c2;
             uint32_t pk[16];
 #if NTB_ATTN_STAGED
             // staged: all 16 scale/subtract FFMA2, then all 2^x, then the
@@ -504,10 +535,10 @@ __global__ void __launch_bounds__(384, 1)
 #endif
             tmem_st_32x32b_x16(t_s + ch * 16, pk);
           }
-          // release this half of P_j to the MMA warp
-          if (half == 1) { TRACE_SM(g, j, 6) }
+          // release this chunk of P_j to the MMA warp
+          if (half == PCH - 1) { TRACE_SM(g, j, 6) }
           tmem_st_wait();
-          if (half == 1) { TRACE_SM(g, j, 7) }
+          if (half == PCH - 1) { TRACE_SM(g, j, 7) }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&p_full[g][half]);
