@@ -168,9 +168,13 @@ class Work:
     """One paper kernel at its BASELINE shape: rotating input sets, the
     public launcher call, algorithmic bytes / flops per call."""
 
-    def __init__(self, name, bound, units, setup, call, check=None, note=""):
+    def __init__(self, name, bound, units, setup, call, check=None, note="", torch_op=None):
         self.name, self.bound, self.units = name, bound, units
         self.setup, self.call, self.check, self.note = setup, call, check, note
+        # (description, fn(set)): the same op through PyTorch's own library
+        # kernels (cuBLAS / cuDNN / flash / ATen), timed the same way - a
+        # library reference point, not the reference implementation
+        self.torch_op = torch_op
 
 
 def _sets_for(bytes_per_set, l2=126e6):
@@ -200,9 +204,13 @@ def build_works(dev, which):
         return s
 
     works["softmax"] = Work("softmax fp16 4096x4096", "hbm", 2 * R * C * 2, rows_setup("softmax"),
-                            lambda a: B.softmax_launch(a["x"], a["y"], C))
+                            lambda a: B.softmax_launch(a["x"], a["y"], C),
+                            torch_op=("torch.softmax(x, -1, out=y)",
+                                      lambda a: torch.softmax(a["x"], -1, out=a["y"])))
     works["rms_norm"] = Work("rms_norm fp16 4096x4096", "hbm", 2 * R * C * 2 + C * 2,
-                             rows_setup("rms"), lambda a: B.rms_norm_launch(a["x"], a["w"], a["y"], C))
+                             rows_setup("rms"), lambda a: B.rms_norm_launch(a["x"], a["w"], a["y"], C),
+                             torch_op=("torch.nn.functional.rms_norm(x, (C,), w, 1e-6)",
+                                       lambda a: torch.nn.functional.rms_norm(a["x"], (C,), a["w"], 1e-6)))
 
     def add_setup(n, dtype):
         def s():
@@ -211,12 +219,15 @@ def build_works(dev, which):
                     for _ in range(k)]
         return s
 
+    t_add = ("torch.add(a, b, out=o)", lambda a: torch.add(a["a"], a["b"], out=a["o"]))
     works["add_2^20"] = Work("add fp32 2^20", "hbm", 3 * 4 * (1 << 20), add_setup(1 << 20, torch.float32),
-                             lambda a: B.add_launch(a["a"], a["b"], a["o"], 1024))
+                             lambda a: B.add_launch(a["a"], a["b"], a["o"], 1024), torch_op=t_add)
     works["add_2^24"] = Work("add fp32 2^24", "hbm", 3 * 4 * (1 << 24), add_setup(1 << 24, torch.float32),
-                             lambda a: B.add_launch(a["a"], a["b"], a["o"], 1024))
+                             lambda a: B.add_launch(a["a"], a["b"], a["o"], 1024), torch_op=t_add)
     works["silu_2^24"] = Work("silu fp16 2^24", "hbm", 2 * 2 * (1 << 24), add_setup(1 << 24, f16),
-                              lambda a: B.silu_launch(a["a"], a["o"], 1024))
+                              lambda a: B.silu_launch(a["a"], a["o"], 1024),
+                              torch_op=("torch.nn.functional.silu(a)",
+                                        lambda a: torch.nn.functional.silu(a["a"])))
     MM = 4096
 
     def mm_setup():
@@ -225,10 +236,15 @@ def build_works(dev, which):
                      d=U((MM, MM))) for _ in range(k)]
 
     works["mm"] = Work("mm fp16 4096^3", "tensor", 2 * MM ** 3, mm_setup,
-                       lambda a: B.mm_launch(a["a"], a["b"], a["c"], 128, 128, 64))
+                       lambda a: B.mm_launch(a["a"], a["b"], a["c"], 128, 128, 64),
+                       torch_op=("torch.mm(a, b, out=c) (cuBLAS)",
+                                 lambda a: torch.mm(a["a"], a["b"], out=a["c"])))
     works["addmm"] = Work("addmm fp16 4096^3", "tensor", 2 * MM ** 3, mm_setup,
                           lambda a: B.addmm_launch(a["d"], a["a"], a["b"], -0.134, -0.201, a["c"],
-                                                   128, 128, 64))
+                                                   128, 128, 64),
+                          torch_op=("torch.addmm(d, a, b, beta, alpha, out=c) (cuBLAS)",
+                                    lambda a: torch.addmm(a["d"], a["a"], a["b"], beta=-0.134,
+                                                          alpha=-0.201, out=a["c"])))
 
     def bmm_setup():
         k = _sets_for(3 * 64 * 1024 * 1024 * 2)
@@ -236,7 +252,9 @@ def build_works(dev, which):
                      c=torch.empty((64, 1024, 1024), device=dev, dtype=f16)) for _ in range(k)]
 
     works["bmm"] = Work("bmm fp16 64x1024^3", "tensor", 2 * 64 * 1024 ** 3, bmm_setup,
-                        lambda a: B.bmm_launch(a["a"], a["b"], a["c"], 128, 128, 64))
+                        lambda a: B.bmm_launch(a["a"], a["b"], a["c"], 128, 128, 64),
+                        torch_op=("torch.bmm(a, b, out=c) (cuBLAS)",
+                                  lambda a: torch.bmm(a["a"], a["b"], out=a["c"])))
 
     def conv_setup():
         k = _sets_for((64 * 256 * 56 * 56 + 64 * 256 * 54 * 54) * 2)
@@ -245,7 +263,9 @@ def build_works(dev, which):
 
     works["conv2d"] = Work("conv2d fp16 N64 C256 56x56 K256 3x3", "tensor",
                            2 * 64 * 54 * 54 * 256 * 256 * 9, conv_setup,
-                           lambda a: B.conv2d_launch(a["x"], a["w"], a["y"], 128, 128, 64))
+                           lambda a: B.conv2d_launch(a["x"], a["w"], a["y"], 128, 128, 64),
+                           torch_op=("torch.nn.functional.conv2d(x, w) (cuDNN, NCHW)",
+                                     lambda a: torch.nn.functional.conv2d(a["x"], a["w"])))
 
     def sdpa_setup():
         shp = (32, 32, 4096, 128)
@@ -253,7 +273,11 @@ def build_works(dev, which):
 
     works["sdpa"] = Work("sdpa fp16 B32 H32 S4096 D128", "tensor", 4 * 32 * 32 * 4096 * 4096 * 128,
                          sdpa_setup, lambda a: B.sdpa_launch(a["q"], a["k"], a["v"], a["o"], 128, 128),
-                         note="single input set (4.3 GB working set >> L2)")
+                         note="single input set (4.3 GB working set >> L2)",
+                         torch_op=("torch.nn.functional.scaled_dot_product_attention(q, k, v) "
+                                   "(PyTorch's fastest available backend)",
+                                   lambda a: torch.nn.functional.scaled_dot_product_attention(
+                                       a["q"], a["k"], a["v"])))
 
     def sdpa_rope_setup():
         shp = (32, 4096, 32, 128)                  # (B, S, H, D) storage, viewed (B, H, S, D)
@@ -306,6 +330,35 @@ def _graph(fn, steps):
         for i in range(steps):
             fn(i)
     return g, B.launch_count() - n0
+
+
+def time_torch_op(work, steps):
+    """The workload's PyTorch library equivalent, timed like time_work
+    (graph of `steps` calls, one replay under CUDA events)."""
+    import torch
+
+    desc, fn = work.torch_op
+    sets = work.setup()
+    for i in range(2):
+        fn(sets[i % len(sets)])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(steps):
+            fn(sets[i % len(sets)])
+    g.replay()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
+    t0.record(stream)
+    g.replay()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    del g, sets
+    torch.cuda.empty_cache()
+    time.sleep(0.5)
+    return desc, ms
 
 
 def time_work(work, steps, warmup, n_gpus):
@@ -676,6 +729,12 @@ def main():
                                 "roofline": roof,
                                 "clocks_under_load": clk,
                                 "note": wk.note}
+                if wk.torch_op is not None and os.environ.get("NTB_BENCH_TORCH", "1") == "1":
+                    desc, tms = time_torch_op(wk, steps)
+                    kernels[key]["torch_same_op"] = {
+                        "what": desc, "ms": round(tms, 5),
+                        "frac": _roofline(wk, tms, pk, None)["frac"],
+                        "ours_speedup": round(tms / ms, 3)}
             except Exception as e:  # report, never hide
                 kernels[key] = {"workload": wk.name, "error": f"{type(e).__name__}: {e}"}
     if rank != 0:
