@@ -81,6 +81,14 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 // flush, so any data dependency is safe) and pdl_trigger() to let their own
 // successor launch early.  Outside a PDL launch both are no-ops.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// L2 prefetch of [p, p + bytes) (bytes a multiple of 16, p 16-byte aligned).
+// Issued BEFORE pdl_wait() it overlaps the DRAM fetch of a kernel's inputs
+// with the previous kernel's tail: L2 is the GPU's point of coherence, so a
+// line the previous kernel still writes is updated in place and the loads
+// after pdl_wait() see the final data.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }

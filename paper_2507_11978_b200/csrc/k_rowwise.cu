@@ -307,13 +307,18 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
   const uint32_t row_bytes = (uint32_t)cols * sizeof(T);
   const uint32_t row_pad = (row_bytes + 127u) & ~127u;
   uint8_t* wbase = smem + (size_t)warp * stages * row_pad;
-  pdl_wait();
-  pdl_trigger();
   // row r goes to CTA r % grid: every SM gets floor or ceil(rows / grid) rows
   // (a block of 16 consecutive rows per CTA gives 4096 rows on 148 SMs as
   // 108 CTAs x 32 rows + 40 x 16 - a 16% longer critical path)
   const int64_t step = (int64_t)gridDim.x * kStreamWarps;
   const int64_t first = (int64_t)blockIdx.x + (int64_t)gridDim.x * warp;
+#if !NTB_ROWS_NO_PREFETCH
+  // the warp's first rows into L2 while the previous kernel drains
+  if (lane < stages && first + lane * step < rows && (row_bytes & 15) == 0)
+    prefetch_l2_bulk(in + (first + lane * step) * in_rs, row_bytes);
+#endif
+  pdl_wait();
+  pdl_trigger();
   // each warp's first row copies are in flight before anything else
   if (lane == 0) {
     for (int s = 0; s < stages; ++s) bar_init(&bars[warp][s], 1);
