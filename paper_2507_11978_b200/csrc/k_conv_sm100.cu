@@ -433,6 +433,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
+#if !NTB_CONV_NO_PDL
+  // programmatic launch (as in the GEMM): the first filter stages go to L2
+  // before waiting for the previous kernel
+  if (warp == 0 && lane == 0 && cid < total) {
+    const int krow = decode(cid).kt * 256 + (int)rank * 128;
+    int n = 0;
+    for (int cbk = 0; cbk < p.cb && n < stages; ++cbk)
+      for (int rs = 0; rs < RS && n < stages; ++rs, ++n) tma_prefetch_3d(&wmap, cbk * BK, rs, krow);
+  }
+  pdl_wait();
+  pdl_trigger();
+#endif
 
   if (warp == 0) {
     if (elect_one()) {
@@ -686,7 +698,11 @@ int launch_conv_fused(const CUtensorMap& wmap, const FusedParams& p, size_t smem
   const int total = p.N * p.pix_tiles * p.k_tiles;
   int clusters = sm_count() / 2;
   if (total < clusters) clusters = total;
+#if NTB_CONV_NO_PDL
   k<<<2 * clusters, kFusedThreads, smem, s>>>(wmap, p);
+#else
+  launch_pdl(k, dim3(2 * clusters), dim3(kFusedThreads), smem, s, wmap, p);
+#endif
 #if NTB_CONV_TRACE
   {
     static long long h[4096];

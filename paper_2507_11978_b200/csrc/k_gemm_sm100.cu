@@ -507,6 +507,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
+#if !NTB_GEMM_NO_PDL
+  // launched with programmatic stream serialization: everything above ran
+  // while the previous kernel drained; the first unit's first K blocks are
+  // requested into L2 before the wait (L2 is coherent with the previous
+  // kernel's writes), then every thread waits for it to complete
+  if (warp == 0 && lane == 0 && cid < units) {
+    int t, half;
+    decode(cid, t, half);
+    const int b = t / tiles_per_batch, r = t % tiles_per_batch;
+    const int nt = r / p.num_m, mt = r % p.num_m;
+    const int row = mt * 256 + (int)rank * 128;
+    const int col = half < 0 ? nt * 256 + (int)rank * 128 : nt * 256 + half * 128 + (int)rank * 64;
+    for (int kb = 0; kb < nk && kb < PSTAGES; ++kb) {
+      if (!A_MN) {
+        tma_prefetch_3d(&maps.a, kb * BK, row, b);
+      } else {
+        tma_prefetch_3d(&maps.a, row, kb * BK, b);
+        tma_prefetch_3d(&maps.a, row + 64, kb * BK, b);
+      }
+      if (!B_MN) {
+        tma_prefetch_3d(&maps.b, kb * BK, col, b);
+      } else {
+        tma_prefetch_3d(&maps.b, col, kb * BK, b);
+        tma_prefetch_3d(&maps.b, col + 64, kb * BK, b);
+      }
+    }
+  }
+  pdl_wait();
+  pdl_trigger();
+#endif
 
   if (warp == 0) {
     if (elect_one()) {
@@ -635,7 +665,11 @@ int launch_pair(const GemmMaps& maps, const GemmParams& p, cudaStream_t s) {
   const int total = p.num_m * p.num_n * p.batch;
   int clusters = sm_count() / 2;
   if (total < clusters) clusters = total;
+#if NTB_GEMM_NO_PDL
   k<<<2 * clusters, 256, PSMEM_BYTES, s>>>(maps, p);
+#else
+  launch_pdl(k, dim3(2 * clusters), dim3(256), PSMEM_BYTES, s, maps, p);
+#endif
   return check_launch("gemm tcgen05 pair", NTB_PATH_GEMM_TC);
 }
 
