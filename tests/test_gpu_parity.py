@@ -552,3 +552,69 @@ def test_verify_simulate_twin(kernel):
         assert float(np.max(np.abs(got.astype(np.float64) - sim), initial=0.0)) <= tol
         done += 1
     assert done == 3
+
+
+def test_pdl_dependent_chains():
+    """Kernels launched with programmatic dependent launch prefetch their
+    first inputs into L2 BEFORE griddepcontrol.wait.  Chains in which every
+    kernel reads the previous kernel's output, queued back to back on one
+    stream (and captured in a CUDA graph), must give bit-identical results
+    to the same chain with a device synchronisation after every launch
+    (L2 is the coherence point; nothing reaches registers or shared memory
+    before the wait).  Outputs are pre-filled with NaN so stale reads show."""
+    torch.manual_seed(0)
+    f16 = torch.float16
+    a = torch.rand(1 << 20, device=DEV)
+    bufs = [a] + [torch.empty_like(a) for _ in range(6)]
+    x = (torch.rand((4096, 4096), device=DEV) * 2 - 1).to(f16)
+    w = (torch.rand(4096, device=DEV) + 0.5).to(f16)
+    rows = [x] + [torch.empty_like(x) for _ in range(4)]
+    m0 = (torch.rand((512, 512), device=DEV) * 2 - 1).to(f16)
+    e = (torch.eye(512, device=DEV) * 0.5).to(f16)
+    mats = [m0] + [torch.empty_like(m0) for _ in range(3)]
+    outs = bufs[1:] + rows[1:] + mats[1:]
+
+    def run(sync):
+        def s():
+            if sync:
+                torch.cuda.synchronize()
+        for i in range(6):
+            backend.add_launch(bufs[i], bufs[i], bufs[i + 1], 1024)
+            s()
+        for i in range(4):
+            if i % 2 == 0:
+                backend.softmax_launch(rows[i], rows[i + 1], 4096)
+            else:
+                backend.rms_norm_launch(rows[i], w, rows[i + 1], 4096)
+            s()
+        for i in range(3):
+            backend.mm_launch(mats[i], e, mats[i + 1], 128, 128, 64)
+            s()
+
+    def nan_fill():
+        for t in outs:
+            t.fill_(float("nan"))
+
+    nan_fill()
+    run(sync=True)
+    torch.cuda.synchronize()
+    expect = [t.clone() for t in outs]
+    assert torch.equal(bufs[6], a * 64)
+    r = m0
+    for _ in range(3):   # one fp16 rounding per step (subnormals round each time)
+        r = (r.float() * 0.5).to(f16)
+    assert torch.equal(mats[3], r)
+    assert bool(torch.isfinite(rows[4]).all())
+    for mode in ("stream", "graph"):
+        nan_fill()
+        if mode == "stream":
+            run(sync=False)
+        else:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                run(sync=False)
+            nan_fill()
+            g.replay()
+        torch.cuda.synchronize()
+        for i, (got, ref) in enumerate(zip(outs, expect)):
+            assert torch.equal(got, ref), (mode, i)
