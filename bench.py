@@ -279,6 +279,18 @@ def build_works(dev, which):
                                    lambda a: torch.nn.functional.scaled_dot_product_attention(
                                        a["q"], a["k"], a["v"])))
 
+    def sdpa_paper_setup():
+        shp = (4, 48, 1024, 64)                    # the paper's sdpa shape
+        k = _sets_for(4 * 4 * 48 * 1024 * 64 * 2)
+        return [dict(q=U(shp), k=U(shp), v=U(shp), o=torch.empty(shp, device=dev, dtype=f16))
+                for _ in range(k)]
+
+    works["sdpa_paper"] = Work(
+        "sdpa fp16 B4 H48 S1024 D64 (the paper's shape)", "tensor", 4 * 4 * 48 * 1024 * 1024 * 64,
+        sdpa_paper_setup, lambda a: B.sdpa_launch(a["q"], a["k"], a["v"], a["o"], 128, 128),
+        torch_op=("torch.nn.functional.scaled_dot_product_attention(q, k, v)",
+                  lambda a: torch.nn.functional.scaled_dot_product_attention(a["q"], a["k"], a["v"])))
+
     def sdpa_rope_setup():
         shp = (32, 4096, 32, 128)                  # (B, S, H, D) storage, viewed (B, H, S, D)
         ang = torch.rand((4096, 64), generator=g, device=dev) * 6 - 3
@@ -708,7 +720,7 @@ def main():
     h = headline(args, n_gpus, rank, pk)
     kernels = {}
     names = ["add_2^20", "add_2^24", "silu_2^24", "softmax", "rms_norm", "mm", "addmm", "bmm",
-             "conv2d", "sdpa", "rope", "sdpa_rope", "rope+sdpa"]
+             "conv2d", "sdpa", "sdpa_paper", "rope", "sdpa_rope", "rope+sdpa"]
     sel = names if args.kernels == "all" else ([] if args.kernels == "none"
                                                else args.kernels.split(","))
     traffic = ncu_traffic()
