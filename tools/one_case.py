@@ -48,3 +48,34 @@ elif kind == "bmm":
         B.bmm_launch(a, b, c, 128, 128, 64)
     torch.cuda.synchronize()
     print("bmm max err", (c[:2].float() - a[:2].float() @ b[:2].float()).abs().max().item())
+elif kind == "rows":
+    r, c = (int(x) for x in sys.argv[2:4])
+    x = T((r, c))
+    w = T((c,))
+    y = torch.zeros_like(x)
+    B.softmax_launch(x, y, c)
+    torch.cuda.synchronize()
+    print("softmax max err", (y.float() - torch.softmax(x.float(), -1)).abs().max().item())
+    B.rms_norm_launch(x, w, y, c)
+    torch.cuda.synchronize()
+    ref = x.float() * torch.rsqrt(x.float().pow(2).mean(-1, keepdim=True) + 1e-6) * w.float()
+    print("rms max err", (y.float() - ref).abs().max().item())
+elif kind == "ew":
+    n = int(sys.argv[2])
+    a, b = T((n,)).float(), T((n,)).float()
+    o = torch.zeros_like(a)
+    B.add_launch(a, b, o, 1024)
+    torch.cuda.synchronize()
+    print("add max err", (o - (a + b)).abs().max().item())
+elif kind == "rope":
+    bb, s, h, d = (int(x) for x in sys.argv[2:6])
+    x = T((bb, s, h, d))
+    ang = torch.rand((s, d // 2), device=dev) * 6 - 3
+    sn, cs = torch.sin(ang).half(), torch.cos(ang).half()
+    o = torch.zeros_like(x)
+    B.rope_launch(x, sn, cs, o, d // 2)
+    torch.cuda.synchronize()
+    x0, x1 = x.float()[..., : d // 2], x.float()[..., d // 2:]
+    c2, s2 = cs.float()[None, :, None, :], sn.float()[None, :, None, :]
+    ref = torch.cat([x0 * c2 - x1 * s2, x0 * s2 + x1 * c2], -1)
+    print("rope max err", (o.float() - ref).abs().max().item())
