@@ -27,7 +27,10 @@ anywhere; ``for`` loops over a nest (ForRange) with loads indexed by the loop
 variable or constants; + - * / max min; exp, sqrt, rsqrt, log, sigmoid, neg,
 abs, tanh, relu; numeric constants; ShapeOf; Zeros; Reduce (max / sum) over
 the WHOLE tile (every other lane axis of extent 1, e.g. softmax / rms_norm-
-style rows); Dot of two (transposed) 2-D operand tiles into the 2-D output
+style rows: element-wise partials + one block reduction) or along ONE axis of
+any loaded tile (results in shared memory, one warp per result element,
+broadcast back with the reference's right-aligned numpy rules, e.g. row sums
+of a (BM, BN) tile stored as (BM,), or x - max(x, axis=0)); Dot of two (transposed) 2-D operand tiles into the 2-D output
 tile - both operands staged in shared memory, fp32 FMA accumulation on the
 CUDA cores (the paper's contractions run on the native tcgen05 kernels; this
 is the path for OTHER contractions, e.g. a matmul with a fused epilogue).
@@ -161,7 +164,23 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
     lane_total = math.prod(uni) if uni else 1
     if lane_total < 1:
         raise CodegenError("empty lane tile")
-    block = 32 * min(8, max(1, math.ceil(lane_total / 32)))
+    def has_reduce(x):
+        if isinstance(x, Reduce):
+            return True
+        return any(has_reduce(c) for c in (getattr(x, "a", None), getattr(x, "b", None))
+                   if c is not None and not isinstance(c, (str, int, float)))
+
+    def stmts_reduce(stmts):
+        for st in stmts:
+            if isinstance(st, ForRange):
+                if stmts_reduce(st.body):
+                    return True
+            elif has_reduce(getattr(st, "expr", None)):
+                return True
+        return False
+    # 8 warps when the program reduces (axis reductions run one warp per result)
+    block = 256 if stmts_reduce(spec.application) else \
+        32 * min(8, max(1, math.ceil(lane_total / 32)))
     per_thread = math.ceil(lane_total / block)
     if per_thread > 64:
         raise CodegenError(f"lane tile of {lane_total} elements is too large for one CTA")
@@ -237,6 +256,85 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
             return "(-INFINITY)" if v < 0 else "INFINITY"
         return f"{v!r}f"
 
+    # -- tile shapes (evaluated), the reference's typecheck rules ------------
+    def bcast(a, b):
+        out = []
+        for i in range(1, max(len(a), len(b)) + 1):
+            da = a[-i] if i <= len(a) else 1
+            db = b[-i] if i <= len(b) else 1
+            if da != db and 1 not in (da, db):
+                raise CodegenError(f"cannot broadcast {tuple(a)} with {tuple(b)}")
+            out.append(db if da == 1 else da)
+        return tuple(reversed(out))
+
+    def shp(x) -> tuple:
+        if isinstance(x, Load):
+            return () if spec.param(x.param).rank == 0 else tuple(ext[x.param])
+        if isinstance(x, Local):
+            k = kind.get(x.name)
+            if isinstance(k, tuple):
+                return k[2]
+            return tuple(uni) if k in ("elem", "elemtmp") else ()
+        if isinstance(x, (ConstF, ShapeOf)):
+            return ()
+        if isinstance(x, Zeros):
+            return tuple(ev(d) for d in x.shape)
+        if isinstance(x, BinOp):
+            return bcast(shp(x.a), shp(x.b))
+        if isinstance(x, UnOp):
+            sa = shp(x.a)
+            return tuple(reversed(sa)) if x.op == "trans" else sa
+        if isinstance(x, Reduce):
+            sa = shp(x.a)
+            return sa[: x.axis] + sa[x.axis + 1:]
+        if isinstance(x, Dot):
+            return tuple(uni)
+        raise CodegenError(f"expression {type(x).__name__}")
+
+    def whole_tile(x: Reduce) -> bool:
+        """The operand is the element universe and every other axis is 1: a
+        row reduction evaluated element-wise + one block reduction."""
+        return list(shp(x.a)) == list(uni) and all(uni[j] == 1 for j in range(nd) if j != x.axis)
+
+    def to_uni(sr) -> bool:
+        """A reduction result right-aligned against the universe (numpy rules)."""
+        if len(sr) > nd:
+            return False
+        o = nd - len(sr)
+        return all(sr[d] in (1, uni[o + d]) for d in range(len(sr)))
+
+    def check_red_operand(y):
+        """Operands of axis reductions are evaluated at explicit coordinates:
+        loads of any lane tile, constants, tile-uniform locals, nested
+        reductions."""
+        if isinstance(y, Load):
+            for n in y.nests:
+                nest_c(n)
+            return
+        if isinstance(y, Local):
+            if kind.get(y.name) != "scalar":
+                raise CodegenError(f"element-wise local {y.name!r} inside an axis reduction")
+            return
+        if isinstance(y, (ConstF, ShapeOf, Zeros)):
+            return
+        if isinstance(y, BinOp):
+            if y.op not in _BIN:
+                raise CodegenError(f"binary op {y.op!r}")
+            check_red_operand(y.a)
+            check_red_operand(y.b)
+            return
+        if isinstance(y, UnOp):
+            if y.op not in _UN:
+                raise CodegenError(f"unary op {y.op!r}")
+            check_red_operand(y.a)
+            return
+        if isinstance(y, Reduce):
+            if y.op not in ("max", "sum"):
+                raise CodegenError(f"reduction {y.op!r}")
+            check_red_operand(y.a)
+            return
+        raise CodegenError(f"{type(y).__name__} inside an axis reduction")
+
     # -- kinds ---------------------------------------------------------------
     def ekind(x) -> str:
         if isinstance(x, Load):
@@ -251,7 +349,8 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
         if isinstance(x, Local):
             if x.name not in kind:
                 raise CodegenError(f"undefined local {x.name!r}")
-            return kind[x.name]
+            k = kind[x.name]
+            return "elem" if isinstance(k, tuple) else k
         if isinstance(x, (ConstF, ShapeOf)):
             return "scalar"
         if isinstance(x, Zeros):
@@ -267,10 +366,17 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
         if isinstance(x, Reduce):
             if x.op not in ("max", "sum"):
                 raise CodegenError(f"reduction {x.op!r}")
-            if any(uni[j] != 1 for j in range(nd) if j != x.axis):
-                raise CodegenError("only whole-tile reductions are generated")
-            ekind(x.a)
-            return "scalar"
+            if whole_tile(x):
+                ekind(x.a)
+                return "scalar"
+            check_red_operand(x.a)
+            sr = shp(x)
+            if all(d == 1 for d in sr):
+                return "scalar"
+            if not to_uni(sr):
+                raise CodegenError(f"reduction result {sr} does not broadcast to the stored "
+                                   f"tile {tuple(uni)}")
+            return "elem"
         if isinstance(x, Dot):
             return "elem"
         raise CodegenError(f"expression {type(x).__name__}")
@@ -291,7 +397,10 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
                  f"{fill(x.other)};")
             return v
         if isinstance(x, Local):
-            return f"v_{x.name}[e]" if kind[x.name] == "elem" else f"v_{x.name}"
+            k = kind[x.name]
+            if isinstance(k, tuple):
+                return red_index(k, lambda j: f"Larr{j}[e]", nd)
+            return f"v_{x.name}[e]" if k == "elem" else f"v_{x.name}"
         if isinstance(x, ConstF):
             return fill(x.value)
         if isinstance(x, Zeros):
@@ -328,6 +437,94 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
         elem_loop(lambda: emit(f"  {r} = {comb.format(a=r, b=expr(inner))};"))
         emit(f"{r} = block_reduce_{x.op}({r}, red);")
         return r
+
+    def red_index(k, coord, ctx_rank):
+        """Element of an axis-reduction result (kind ("red", array, shape)) at
+        context coordinates coord(j), right-aligned (numpy broadcasting)."""
+        _, arr, sr = k
+        o = ctx_rank - len(sr)
+        terms = []
+        for d in range(len(sr)):
+            if sr[d] == 1:
+                continue
+            stride = math.prod(sr[d + 1:]) if d + 1 < len(sr) else 1
+            terms.append(f"(int)({coord(o + d)}) * {stride}")
+        return f"{arr}[{' + '.join(terms) if terms else '0'}]"
+
+    def expr_at(y, coord, ctx) -> str:
+        """C float expression of y at context coordinates coord(j) of a
+        context tile of shape ctx (y broadcasts into ctx, right-aligned)."""
+        if isinstance(y, Load):
+            if spec.param(y.param).rank == 0:
+                return f"s_{y.param}"
+            e = ext[y.param]
+            o = len(ctx) - len(e)
+            if o < 0:
+                raise CodegenError(f"{y.param!r} tile {e} inside a context tile {ctx}")
+            lane = (lambda j: "((i64)0)" if e[j] == 1 else f"((i64)({coord(o + j)}))")
+            off, mask = off_mask(y.param, map_sym(y.param, y.nests, lane))
+            v = fresh()
+            emit(f"const float {v} = ({mask}) ? to_f(p{tnames.index(y.param)}[{off}]) : "
+                 f"{fill(y.other)};")
+            return v
+        if isinstance(y, Local):
+            k = kind[y.name]
+            if isinstance(k, tuple):
+                return red_index(k, coord, len(ctx))
+            if k != "scalar":
+                raise CodegenError(f"element-wise local {y.name!r} inside an axis reduction")
+            return f"v_{y.name}"
+        if isinstance(y, (ConstF, Zeros, ShapeOf)):
+            return expr(y)
+        if isinstance(y, BinOp):
+            return _BIN[y.op].format(a=expr_at(y.a, coord, ctx), b=expr_at(y.b, coord, ctx))
+        if isinstance(y, UnOp):
+            return _UN[y.op].format(a=expr_at(y.a, coord, ctx))
+        raise CodegenError(f"{type(y).__name__} inside an axis reduction")
+
+    def axis_reduce_code(x: Reduce):
+        """Reduction along one axis of a tile that is not the element universe
+        (e.g. row sums of a (BM, BN) tile stored as (BM,), or column maxima
+        broadcast back over rows): the results go to shared memory, one warp
+        per result element, lanes striding the reduced axis."""
+        inner = hoist(x.a)          # nested reductions first
+        sa = shp(inner)
+        ax = x.axis
+        sr = sa[:ax] + sa[ax + 1:]
+        nres = math.prod(sr) if sr else 1
+        if smem_bytes[0] + 4 * nres > 46 * 1024:
+            raise CodegenError(f"reduction result of {nres} elements exceeds the generic path's "
+                               "shared-memory budget")
+        smem_bytes[0] += 4 * nres
+        n = fresh()
+        arr = f"R{n}"
+        shared_decls.append(f"  __shared__ float {arr}[{nres}];")
+        ident = "(-INFINITY)" if x.op == "max" else "0.0f"
+        comb = "fmaxf({a}, {b})" if x.op == "max" else "({a} + {b})"
+        shfl = "fmaxf(a_, __shfl_xor_sync(0xffffffffu, a_, o_))" if x.op == "max" else \
+               "a_ + __shfl_xor_sync(0xffffffffu, a_, o_)"
+        emit("__syncthreads();")
+        emit(f"for (int r_ = threadIdx.x >> 5; r_ < {nres}; r_ += NT / 32) {{")
+        ind[0] += "  "
+        rc = []
+        for d in range(len(sr)):
+            stride = math.prod(sr[d + 1:]) if d + 1 < len(sr) else 1
+            emit(f"const int {n}_c{d} = (r_ / {stride}) % {sr[d]};")
+            rc.append(f"{n}_c{d}")
+        coords = rc[:ax] + ["k_"] + rc[ax:]
+        emit(f"float a_ = {ident};")
+        emit(f"for (int k_ = threadIdx.x & 31; k_ < {sa[ax]}; k_ += 32) {{")
+        ind[0] += "  "
+        val = expr_at(inner, lambda j: coords[j], sa)
+        emit(f"a_ = {comb.format(a='a_', b=val)};")
+        ind[0] = ind[0][:-2]
+        emit("}")
+        emit(f"for (int o_ = 16; o_; o_ >>= 1) a_ = {shfl};")
+        emit(f"if ((threadIdx.x & 31) == 0) {arr}[r_] = a_;")
+        ind[0] = ind[0][:-2]
+        emit("}")
+        emit("__syncthreads();")
+        return ("red", arr, tuple(sr))
 
     def operand(x):
         """(Load, transposed) of a dot operand."""
@@ -391,8 +588,16 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
         """Evaluate reductions and dots first; return an element expression."""
         if isinstance(x, Reduce):
             name = fresh()
-            emit(f"const float v_{name} = {reduce_code(x)};")
-            kind[name] = "scalar"
+            if whole_tile(x):
+                emit(f"const float v_{name} = {reduce_code(x)};")
+                kind[name] = "scalar"
+                return Local(name)
+            k = axis_reduce_code(x)
+            if all(d == 1 for d in k[2]):
+                emit(f"const float v_{name} = {k[1]}[0];")
+                kind[name] = "scalar"
+            else:
+                kind[name] = k
             return Local(name)
         if isinstance(x, Dot):
             t = dot_code(x)
@@ -407,7 +612,9 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
 
     def scalar_expr(x) -> str:
         if isinstance(x, Reduce):
-            return reduce_code(x)
+            if whole_tile(x):
+                return reduce_code(x)
+            return f"{axis_reduce_code(x)[1]}[0]"
         if isinstance(x, BinOp):
             return _BIN[x.op].format(a=scalar_expr(x.a), b=scalar_expr(x.b))
         if isinstance(x, UnOp):

@@ -123,14 +123,16 @@ def test_non_catalog_spec_takes_the_generic_path_and_needs_cuda_tensors():
 
 
 def test_spec_outside_generic_subset_is_unsupported():
-    """Row-wise (not whole-tile) reductions are neither a native family nor
-    generated: UnsupportedSpecError names the reason."""
-    from paper_2507_11978_b200.spec import (ArrangeOp, BinOp, KernelSpec, Load, ParamSpec, Reduce,
-                                            Store, typecheck)
+    """A contraction whose operand is an expression (not a loaded tile) is
+    neither a native family nor generated: UnsupportedSpecError names the
+    reason."""
+    from paper_2507_11978_b200.spec import (ArrangeOp, BinOp, ConstF, Dot, KernelSpec, Load,
+                                            ParamSpec, Store, typecheck)
     t = (ArrangeOp("tile", shape=(S.var("B"), S.var("B"))),)
-    spec = KernelSpec("rowcenter", (ParamSpec("a", 2, "f16", "in"), ParamSpec("c", 2, "f16", "out")),
+    spec = KernelSpec("dot_of_expr", (ParamSpec("a", 2, "f16", "in"),
+                                      ParamSpec("c", 2, "f16", "out")),
                       ("B",), {"a": t, "c": t},
-                      (Store("c", BinOp("-", Load("a"), Reduce("sum", 1, Load("a")))),))
+                      (Store("c", Dot(BinOp("*", Load("a"), ConstF(2.0)), Load("a"))),))
     with pytest.raises(backend.UnsupportedSpecError, match="generic path"):
         backend.launch(typecheck(spec), {"a": _Fake((8, 8)), "c": _Fake((8, 8))}, {"B": 4})
 

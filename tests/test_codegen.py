@@ -79,6 +79,44 @@ def mm_relu_kernel():
     return make(arrangement, application, (Tensor(2), Tensor(2), Tensor(2)))
 
 
+def rowsum_kernel():
+    """Row sums of a (BM, BN) tile stored as a (BM,) tile: a reduction along
+    one axis of a tile larger than the stored one."""
+    def arrangement(x, out, BM=BM, BN=BN):
+        return x.tile((BM, BN)).squeeze(1), out.tile((BM,))
+
+    def application(x, out):
+        out = ntl.sum(x, axis=1)  # noqa: F841
+
+    return make(arrangement, application, (Tensor(2), Tensor(1)))
+
+
+def colnorm_kernel():
+    """x - max(x, axis=0): column maxima broadcast back over the rows."""
+    def arrangement(x, out, BM=BM, BN=BN):
+        return x.tile((BM, BN)), out.tile((BM, BN))
+
+    def application(x, out):
+        out = ntl.exp(x - ntl.max(x, axis=0))  # noqa: F841
+
+    return make(arrangement, application, (Tensor(2, other=float("-inf")), Tensor(2)))
+
+
+def rowcenter_kernel():
+    """a - sum(a, axis=1) on a square tile: the (B,) row sums broadcast
+    right-aligned, i.e. along the LAST axis (the reference's numpy rules,
+    tileir.py:290-306) - out[i][j] = a[i][j] - sum_k a[j][k]."""
+    B = Symbol("B", constexpr=True)
+
+    def arrangement(a, c, B=B):
+        return a.tile((B, B)), c.tile((B, B))
+
+    def application(a, c):
+        c = a - ntl.sum(a, axis=1)  # noqa: F841
+
+    return make(arrangement, application, (Tensor(2), Tensor(2)))
+
+
 def _binding(k, shapes, meta):
     b = dict(meta)
     for p, shp in zip(k.checked.spec.params, shapes):
@@ -98,6 +136,9 @@ CASES = [
     (temp_softmax_kernel, [(33, 1000)] * 2, {"BLOCK": 1024}),
     (l2norm_kernel, [(7, 4096)] * 2, {"BLOCK": 4096}),
     (mm_relu_kernel, [(200, 96), (96, 130), (200, 130)], {"BM": 32, "BN": 32, "BK": 32}),
+    (rowsum_kernel, [(100, 300), (100,)], {"BM": 16, "BN": 512}),
+    (colnorm_kernel, [(100, 300)] * 2, {"BM": 64, "BN": 32}),
+    (rowcenter_kernel, [(40, 40)] * 2, {"B": 16}),
 ]
 
 
@@ -191,3 +232,41 @@ def test_generic_contraction_on_b200():
         ref = np.maximum(ta.float().cpu().numpy() @ tb.float().cpu().numpy(), 0)
         tol = 1e-4 if dt == torch.float32 else 1e-2
         np.testing.assert_allclose(out.float().cpu().numpy(), ref, rtol=tol, atol=tol)
+
+
+@pytest.mark.gpu
+def test_generic_axis_reductions_on_b200():
+    """Reductions along one axis of a loaded tile (results in shared memory,
+    broadcast with the reference's rules) against numpy on the same
+    fp16-rounded inputs."""
+    import torch
+
+    rng = np.random.default_rng(4)
+    x = rng.uniform(-1, 1, (100, 300)).astype(np.float32)
+    for dt, tol in ((torch.float32, 1e-5), (torch.float16, 1e-2)):
+        tx = torch.from_numpy(x).cuda().to(dt)
+        out = torch.empty(100, device="cuda", dtype=dt)
+        before = backend.path_counts()["jit"]
+        rowsum_kernel()(tx, out, BM=16, BN=512)
+        torch.cuda.synchronize()
+        assert backend.path_counts()["jit"] == before + 1
+        ref = tx.float().cpu().numpy().sum(1)
+        np.testing.assert_allclose(out.float().cpu().numpy(), ref, rtol=tol, atol=tol)
+        (xin,), got = _run(colnorm_kernel(), [x], {"BM": 64, "BN": 32}, dt)
+        # per program: the column maximum over that program's 64 rows
+        ref = np.empty_like(xin)
+        for r0 in range(0, 100, 64):
+            blk = xin[r0:r0 + 64]
+            ref[r0:r0 + 64] = np.exp(blk - blk.max(0, keepdims=True))
+        np.testing.assert_allclose(got, ref, rtol=tol, atol=tol)
+    a = rng.uniform(-1, 1, (40, 40)).astype(np.float32)
+    (ain,), got = _run(rowcenter_kernel(), [a], {"B": 16}, torch.float32)
+    ref = np.empty_like(ain)
+    for i0 in range(0, 40, 16):
+        for j0 in range(0, 40, 16):
+            t = np.zeros((16, 16), np.float32)
+            blk = ain[i0:i0 + 16, j0:j0 + 16]
+            t[:blk.shape[0], :blk.shape[1]] = blk          # masked loads read 0
+            r = t - t.sum(1)                                # (16,) broadcast over rows
+            ref[i0:i0 + 16, j0:j0 + 16] = r[:blk.shape[0], :blk.shape[1]]
+    np.testing.assert_allclose(got, ref, rtol=1e-5, atol=1e-5)
