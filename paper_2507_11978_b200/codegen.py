@@ -22,8 +22,8 @@ Execution model (one CTA per program, the reference's program = one tile):
   ``%`` (symexpr.py:31-161), float math is fp32, loads/stores convert from /
   to the tensor dtype (f32, f16, bf16).
 
-Supported application IR: Let / Store at the top level, Assign / Accumulate
-anywhere; ``for`` loops over a nest (ForRange) with loads indexed by the loop
+Supported application IR: Store at the top level (the reference forbids
+stores in loops, tileir.py:425-426), Let / Assign / Accumulate anywhere; ``for`` loops over a nest (ForRange) with loads indexed by the loop
 variable or constants; + - * / max min; exp, sqrt, rsqrt, log, sigmoid, neg,
 abs, tanh, relu; numeric constants; ShapeOf; Zeros; Reduce (max / sum) over
 the WHOLE tile (every other lane axis of extent 1, e.g. softmax / rms_norm-
@@ -651,8 +651,8 @@ def generate(checked, binding: dict, dtype: int) -> Generated:
             elif isinstance(st, (Let, Assign, Accumulate)):
                 k = ekind(st.expr)
                 if isinstance(st, Let):
-                    if not top:
-                        raise CodegenError("declarations inside loops are not generated")
+                    # inside a loop the C declaration is scoped to the loop
+                    # body: a fresh binding per iteration, as in the sim
                     kind[st.name] = k
                     if k == "elem":
                         emit(f"float v_{st.name}[E];")

@@ -117,6 +117,26 @@ def rowcenter_kernel():
     return make(arrangement, application, (Tensor(2), Tensor(2)))
 
 
+def mm_scaled_kernel():
+    """A local declared inside the K loop (fresh binding per iteration)."""
+    def arrangement(input, other, output, BM=BM, BN=BN, BK=BK):
+        output_tiled = output.tile((BM, BN))
+        input_tiled = input.tile((BM, BK)).tile((1, -1)).expand((-1, output_tiled.shape[1]))
+        input_tiled.dtype = input_tiled.dtype.squeeze(0)
+        other_tiled = other.tile((BK, BN)).tile((-1, 1)).expand((output_tiled.shape[0], -1))
+        other_tiled.dtype = other_tiled.dtype.squeeze(1)
+        return input_tiled, other_tiled, output_tiled
+
+    def application(input, other, output):
+        accumulator = ntl.zeros(output.shape, dtype=ntl.float32)
+        for k in range(input.shape[0]):
+            part = ntl.dot(input[k], other[k])
+            accumulator += part * 0.5
+        output = accumulator  # noqa: F841
+
+    return make(arrangement, application, (Tensor(2), Tensor(2), Tensor(2)))
+
+
 def _binding(k, shapes, meta):
     b = dict(meta)
     for p, shp in zip(k.checked.spec.params, shapes):
@@ -136,6 +156,7 @@ CASES = [
     (temp_softmax_kernel, [(33, 1000)] * 2, {"BLOCK": 1024}),
     (l2norm_kernel, [(7, 4096)] * 2, {"BLOCK": 4096}),
     (mm_relu_kernel, [(200, 96), (96, 130), (200, 130)], {"BM": 32, "BN": 32, "BK": 32}),
+    (mm_scaled_kernel, [(200, 96), (96, 130), (200, 130)], {"BM": 32, "BN": 32, "BK": 32}),
     (rowsum_kernel, [(100, 300), (100,)], {"BM": 16, "BN": 512}),
     (colnorm_kernel, [(100, 300)] * 2, {"BM": 64, "BN": 32}),
     (rowcenter_kernel, [(40, 40)] * 2, {"B": 16}),
@@ -270,3 +291,17 @@ def test_generic_axis_reductions_on_b200():
             r = t - t.sum(1)                                # (16,) broadcast over rows
             ref[i0:i0 + 16, j0:j0 + 16] = r[:blk.shape[0], :blk.shape[1]]
     np.testing.assert_allclose(got, ref, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.gpu
+def test_generic_loop_local_on_b200():
+    import torch
+
+    rng = np.random.default_rng(5)
+    a = rng.uniform(-1, 1, (200, 96)).astype(np.float32)
+    b = rng.uniform(-1, 1, (96, 130)).astype(np.float32)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    out = torch.empty((200, 130), device="cuda")
+    mm_scaled_kernel()(ta, tb, out, BM=32, BN=32, BK=32)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(out.cpu().numpy(), 0.5 * (a @ b), rtol=1e-4, atol=1e-4)
