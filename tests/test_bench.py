@@ -1,0 +1,56 @@
+"""bench.py contract on CPU: the reference arm (the oracle port timed on the
+host) prints the driver's JSON line, and the roofline / L2-rotation helpers
+compute what DESIGN.md section 6 says.  The device arm needs a B200."""
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["metric"] == bench.METRIC
+    assert line["steps"] == 1 and line["warmup"] == 3 and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] in ("port", "reference")
+    assert line["cpu_baseline"]["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_roofline_fraction():
+    w = bench.Work("x", "hbm", 1e9, None, None)
+    r = bench._roofline(w, 1.0, {"hbm": 2000.0, "tc": 1000.0}, 123)
+    assert r["achieved"] == pytest.approx(1000.0) and r["frac"] == pytest.approx(0.5)
+    assert r["unit"] == "GB/s" and r["traffic"] == 123
+    w = bench.Work("y", "tensor", 2e12, None, None)
+    r = bench._roofline(w, 2.0, {"hbm": 2000.0, "tc": 1000.0}, None)
+    assert r["achieved"] == pytest.approx(1000.0) and r["frac"] == pytest.approx(1.0)
+    assert r["unit"] == "TFLOP/s"
+
+
+def test_rotating_sets_exceed_l2():
+    # enough input/output sets that consecutive launches never hit in L2
+    for b in (12_582_912, 67_108_864, 134_225_920, 2_148_532_224):
+        n = bench._sets_for(b)
+        assert n >= 2 and n * b >= 3 * 126e6 or n == 2
+
+
+def test_peaks_and_traffic_files():
+    pk = bench.peaks()
+    assert pk["hbm"] > 0 and pk["tc"] > 0
+    tr = bench.ncu_traffic()
+    assert all(v > 0 for k, v in tr.items() if not k.startswith("_"))
