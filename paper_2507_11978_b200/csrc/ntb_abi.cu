@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 
 #include "mapvm.cuh"
@@ -49,23 +50,34 @@ int sm_count() {
   return cached[dev];
 }
 
+// Library-owned scratch (conv's repacked filter + image, sdpa_rope's rotated
+// K) is kept PER STREAM: within a stream, reuse is ordered by the stream;
+// two streams never share a buffer.  Growth frees the old buffer after a
+// device-wide sync (cudaFree), so no in-flight kernel still reads it.
+struct Ws {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
 static std::mutex g_ws_mu;
-static void* g_ws = nullptr;
-static size_t g_ws_bytes = 0;
+static std::unordered_map<cudaStream_t, Ws> g_ws;
 
 void* workspace(size_t bytes, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  if (bytes > g_ws_bytes) {
-    if (g_ws) {
+  Ws& w = g_ws[s];
+  if (bytes > w.bytes) {
+    if (w.p) {
       cudaStreamSynchronize(s);
-      cudaFree(g_ws);
+      cudaFree(w.p);
     }
-    g_ws = nullptr;
-    g_ws_bytes = 0;
-    if (cudaMalloc(&g_ws, bytes) != cudaSuccess) return nullptr;
-    g_ws_bytes = bytes;
+    w.p = nullptr;
+    w.bytes = 0;
+    if (cudaMalloc(&w.p, bytes) != cudaSuccess) {
+      w.p = nullptr;
+      return nullptr;
+    }
+    w.bytes = bytes;
   }
-  return g_ws;
+  return w.p;
 }
 
 // ---- GPU probe: one thread per (pid, nest, lane) point -------------------
@@ -307,9 +319,9 @@ int ntb_launch(int kernel, int dtype, void* const* ptrs, int n_ptrs, const doubl
 
 int ntb_release_workspace(void) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  if (g_ws) cudaFree(g_ws);
-  g_ws = nullptr;
-  g_ws_bytes = 0;
+  for (auto& kv : g_ws)
+    if (kv.second.p) cudaFree(kv.second.p);
+  g_ws.clear();
   return NTB_OK;
 }
 

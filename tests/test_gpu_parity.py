@@ -618,3 +618,47 @@ def test_pdl_dependent_chains():
         torch.cuda.synchronize()
         for i, (got, ref) in enumerate(zip(outs, expect)):
             assert torch.equal(got, ref), (mode, i)
+
+
+def test_workspace_is_per_stream():
+    """Library scratch (conv's repacked filter + image, sdpa_rope's rotated
+    K) is per stream: the same ops queued concurrently on two streams give
+    the results of running them one at a time."""
+    f16 = torch.float16
+    g = torch.Generator(device=DEV).manual_seed(7)
+
+    def U(*shape):
+        return (torch.rand(shape, generator=g, device=DEV) * 2 - 1).to(f16)
+
+    def rope_case():
+        b, s, h, d = 2, 512, 4, 128
+        q, k, v = U(b, s, h, d), U(b, s, h, d), U(b, s, h, d)
+        ang = torch.rand((s, d // 2), generator=g, device=DEV) * 6 - 3
+        sn, cs = torch.sin(ang).to(f16), torch.cos(ang).to(f16)
+        o = torch.empty((b, h, s, d), device=DEV, dtype=f16)
+        return (q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), sn, cs, sn, cs, o)
+
+    def conv_case():
+        x, w = U(2, 64, 20, 20), U(128, 64, 3, 3)
+        return (x, w, torch.empty((2, 128, 18, 18), device=DEV, dtype=f16))
+
+    cases = [(rope_case(), lambda a: backend.sdpa_rope_launch(*a, 128, 128)),
+             (rope_case(), lambda a: backend.sdpa_rope_launch(*a, 128, 128)),
+             (conv_case(), lambda a: backend.conv2d_launch(*a, 128, 128, 64)),
+             (conv_case(), lambda a: backend.conv2d_launch(*a, 128, 128, 64))]
+    expect = []
+    for args, fn in cases:                       # one at a time
+        fn(args)
+        torch.cuda.synchronize()
+        expect.append(args[-1].clone())
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    for _ in range(3):
+        for args, _fn in cases:
+            args[-1].fill_(float("nan"))
+        torch.cuda.synchronize()
+        for i, (args, fn) in enumerate(cases):   # interleaved on two streams
+            with torch.cuda.stream(streams[i % 2]):
+                fn(args)
+        torch.cuda.synchronize()
+        for (args, _fn), ref in zip(cases, expect):
+            assert torch.equal(args[-1], ref)
