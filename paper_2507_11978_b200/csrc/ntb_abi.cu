@@ -5,7 +5,8 @@
 
 #include <atomic>
 #include <mutex>
-#include <unordered_map>
+#include <map>
+#include <utility>
 #include <string>
 
 #include "mapvm.cuh"
@@ -59,11 +60,14 @@ struct Ws {
   size_t bytes = 0;
 };
 static std::mutex g_ws_mu;
-static std::unordered_map<cudaStream_t, Ws> g_ws;
+// keyed by (device, stream): the legacy default stream is per device
+static std::map<std::pair<int, cudaStream_t>, Ws> g_ws;
 
 void* workspace(size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  Ws& w = g_ws[s];
+  Ws& w = g_ws[{dev, s}];
   if (bytes > w.bytes) {
     if (w.p) {
       cudaStreamSynchronize(s);
@@ -319,8 +323,14 @@ int ntb_launch(int kernel, int dtype, void* const* ptrs, int n_ptrs, const doubl
 
 int ntb_release_workspace(void) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
   for (auto& kv : g_ws)
-    if (kv.second.p) cudaFree(kv.second.p);
+    if (kv.second.p) {
+      cudaSetDevice(kv.first.first);
+      cudaFree(kv.second.p);
+    }
+  cudaSetDevice(cur);
   g_ws.clear();
   return NTB_OK;
 }
