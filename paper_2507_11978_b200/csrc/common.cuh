@@ -111,4 +111,18 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 inline int64_t cdiv64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Raise a kernel's dynamic shared-memory limit once per device (function
+// attributes are per device context; a process may drive several GPUs).
+constexpr int kMaxDevices = 64;
+template <typename Kern>
+inline cudaError_t smem_attr_once(Kern k, size_t bytes, size_t (&done)[kMaxDevices]) {
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d >= 0 && d < kMaxDevices && bytes <= done[d]) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && d >= 0 && d < kMaxDevices) done[d] = bytes;
+  return e;
+}
+
 }  // namespace ntb

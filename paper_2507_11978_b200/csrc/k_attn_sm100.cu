@@ -599,12 +599,9 @@ template <int D, bool BF16, bool ROPE>
 int launch_attn(const AttnMaps& maps, const AttnParams& p, cudaStream_t s) {
   using L = Layout<D, ROPE>;
   auto k = attn_fwd_kernel<D, BF16, ROPE>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-    if (e != cudaSuccess) return cuda_fail(e, "attention smem attribute");
-    attr_set = true;
-  }
+  static size_t attr[kMaxDevices] = {};
+  cudaError_t e = smem_attr_once(k, L::SMEM, attr);
+  if (e != cudaSuccess) return cuda_fail(e, "attention smem attribute");
   const int grid = p.n_items < sm_count() ? p.n_items : sm_count();
   k<<<grid, 384, L::SMEM, s>>>(maps, p);
 #if NTB_ATTN_TRACE

@@ -309,12 +309,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 template <bool BF16>
 int launch_conv(const ConvMaps& maps, const ConvParams& p, cudaStream_t s) {
   auto k = conv_pair_kernel<BF16>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e, "conv smem attribute");
-    attr_set = true;
-  }
+  static size_t attr[kMaxDevices] = {};
+  cudaError_t e = smem_attr_once(k, SMEM_BYTES, attr);
+  if (e != cudaSuccess) return cuda_fail(e, "conv smem attribute");
   const int total = p.N * p.pix_tiles * p.k_tiles;
   int clusters = sm_count() / 2;
   if (total < clusters) clusters = total;
@@ -689,12 +686,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
 template <bool BF16, int TN>
 int launch_conv_fused(const CUtensorMap& wmap, const FusedParams& p, size_t smem, cudaStream_t s) {
   auto k = conv_fused_kernel<BF16, TN>;
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_fail(e, "conv fused smem attribute");
-    attr = smem;
-  }
+  static size_t attr[kMaxDevices] = {};
+  cudaError_t e = smem_attr_once(k, smem, attr);
+  if (e != cudaSuccess) return cuda_fail(e, "conv fused smem attribute");
   const int total = p.N * p.pix_tiles * p.k_tiles;
   int clusters = sm_count() / 2;
   if (total < clusters) clusters = total;

@@ -310,12 +310,9 @@ __global__ void __launch_bounds__(256, 1)
 template <bool A_MN, bool B_MN, bool BF16>
 int launch_tc(const GemmMaps& maps, const GemmParams& p, cudaStream_t s) {
   auto k = gemm_tc_kernel<A_MN, B_MN, BF16>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e, "gemm smem attribute");
-    attr_set = true;
-  }
+  static size_t attr[kMaxDevices] = {};
+  cudaError_t e = smem_attr_once(k, SMEM_BYTES, attr);
+  if (e != cudaSuccess) return cuda_fail(e, "gemm smem attribute");
   const int total = p.num_m * p.num_n * p.batch;
   int grid = sm_count();
   if (total < grid) grid = total;
@@ -656,12 +653,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 template <bool A_MN, bool B_MN, bool BF16>
 int launch_pair(const GemmMaps& maps, const GemmParams& p, cudaStream_t s) {
   auto k = gemm_pair_kernel<A_MN, B_MN, BF16>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PSMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e, "gemm pair smem attribute");
-    attr_set = true;
-  }
+  static size_t attr[kMaxDevices] = {};
+  cudaError_t e = smem_attr_once(k, PSMEM_BYTES, attr);
+  if (e != cudaSuccess) return cuda_fail(e, "gemm pair smem attribute");
   const int total = p.num_m * p.num_n * p.batch;
   int clusters = sm_count() / 2;
   if (total < clusters) clusters = total;

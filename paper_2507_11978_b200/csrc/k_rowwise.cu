@@ -464,13 +464,8 @@ static bool try_stream(const T* in, int64_t in_rs, const T* w, T* out, int64_t o
   if (stages < 1) return false;
   const size_t smem = (size_t)(kStreamWarps * stages * row_pad + (kSoftmax ? 0 : row_pad));
   auto kern = row_stream_kernel<T, kSoftmax>;
-  static size_t attr = 0;
-  if (smem > attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return false;
-    attr = smem;
-  }
+  static size_t attr[kMaxDevices] = {};
+  if (smem_attr_once(kern, smem, attr) != cudaSuccess) return false;
   int64_t blocks = cdiv64(rows, kStreamWarps);
   if (blocks > sm_count()) blocks = sm_count();
   launch_pdl(kern, dim3((unsigned)blocks), dim3(kStreamWarps * 32), smem, s, in, in_rs, w, out,
