@@ -41,7 +41,11 @@ namespace ntb {
 namespace {
 
 constexpr int BK = 64;
-constexpr int STAGES = 6;
+constexpr int STAGES = 6;          // unfused (NHWC / TMA image) kernel
+#ifndef NTB_CONV_FSTAGES
+#define NTB_CONV_FSTAGES 6
+#endif
+constexpr int FSTAGES = NTB_CONV_FSTAGES;   // fused kernel's filter ring (max)
 constexpr int A_BYTES = 128 * BK * 2;
 constexpr int B_BYTES = 128 * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -377,7 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFusedThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sWin = smem + p.stages * A_BYTES;
   __shared__ float xpose[4 * XPOSE_FLOATS];
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2], wfull[2],
+  __shared__ __align__(8) uint64_t full[FSTAGES], empty[FSTAGES], tfull[2], tempty[2], wfull[2],
       wempty[2];
   __shared__ uint32_t tmem_slot;
 
@@ -773,7 +777,7 @@ int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s) {
     const int64_t win_rows = ((TN / 2 + (c.R - 1) * c.W + (c.S - 1)) + 15) / 16 * 16;
     const size_t budget = 227 * 1024 - sizeof(float) * 4 * XPOSE_FLOATS - 512 - 1024;
     const size_t win_bytes = (size_t)win_rows * 128;
-    int stages = STAGES;
+    int stages = FSTAGES;
     while (stages >= 3 && (size_t)stages * A_BYTES + 2 * win_bytes > budget) --stages;
     if (stages >= 3 && !getenv("NTB_CONV_UNFUSED")) {
       CUtensorMap wmap;

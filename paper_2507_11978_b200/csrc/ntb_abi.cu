@@ -53,7 +53,8 @@ int sm_count() {
 
 // Library-owned scratch (conv's repacked filter + image, sdpa_rope's rotated
 // K) is kept PER STREAM: within a stream, reuse is ordered by the stream;
-// two streams never share a buffer.  Growth frees the old buffer after a
+// two streams never share a buffer (except inside a CUDA-graph capture, see
+// below).  Growth frees the old buffer after a
 // device-wide sync (cudaFree), so no in-flight kernel still reads it.
 struct Ws {
   void* p = nullptr;
@@ -67,6 +68,21 @@ void* workspace(size_t bytes, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_ws_mu);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  if (cap != cudaStreamCaptureStatusNone) {
+    // CUDA-graph capture (often on a side stream): no allocation or sync is
+    // legal here, so the graph bakes in this device's largest workspace -
+    // run the op once outside capture first (warm-up) to size it
+    auto it = g_ws.find({dev, s});
+    if (it != g_ws.end() && it->second.bytes >= bytes) return it->second.p;
+    Ws* best = nullptr;
+    for (auto& kv : g_ws)
+      if (kv.first.first == dev && kv.second.bytes >= bytes &&
+          (!best || kv.second.bytes > best->bytes))
+        best = &kv.second;
+    return best ? best->p : nullptr;
+  }
   Ws& w = g_ws[{dev, s}];
   if (bytes > w.bytes) {
     if (w.p) {

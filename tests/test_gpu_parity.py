@@ -623,7 +623,8 @@ def test_pdl_dependent_chains():
 def test_workspace_is_per_stream():
     """Library scratch (conv's repacked filter + image, sdpa_rope's rotated
     K) is per stream: the same ops queued concurrently on two streams give
-    the results of running them one at a time."""
+    the results of running them one at a time; and they can be captured in
+    a CUDA graph after a warm-up."""
     f16 = torch.float16
     g = torch.Generator(device=DEV).manual_seed(7)
 
@@ -662,3 +663,15 @@ def test_workspace_is_per_stream():
         torch.cuda.synchronize()
         for (args, _fn), ref in zip(cases, expect):
             assert torch.equal(args[-1], ref)
+    # CUDA-graph capture (torch captures on a side stream): after the warm-up
+    # above, the captured ops reuse the device's workspace without allocating
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for args, fn in cases:
+            fn(args)
+    for args, _fn in cases:
+        args[-1].fill_(float("nan"))
+    graph.replay()
+    torch.cuda.synchronize()
+    for (args, _fn), ref in zip(cases, expect):
+        assert torch.equal(args[-1], ref)
