@@ -58,6 +58,10 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int PCH = NTB_ATTN_PCH;
 static_assert(PCH == 2 || PCH == 4, "P chunks");
 
+#ifndef NTB_ATTN_PBUF
+#define NTB_ATTN_PBUF 1  // D = 64: P in its own TMEM columns, S_{j+1} issued during softmax_j
+#endif
+
 #ifndef NTB_ATTN_TRACE
 #define NTB_ATTN_TRACE 0  // debug builds: per-phase clock64 stamps of CTA 0's first item
 #endif
@@ -181,6 +185,12 @@ struct Layout {
   static constexpr int SMEM = OFF_KV + NS * SLOT + 1024;
   static constexpr uint32_t T_S0 = 0, T_S1 = BN, T_O0 = 2 * BN, T_O1 = 2 * BN + D;
   static_assert(2 * BN + 2 * D <= 512, "TMEM budget");
+  // D = 64 leaves 128 TMEM columns: each query tile gets its own P buffer
+  // (BN/2 columns of packed 16-bit P), so S_{j+1} can overwrite the S
+  // columns as soon as the softmax has read S_j - no wait for P.V + S
+  static constexpr bool SEP_P = NTB_ATTN_PBUF && 2 * BN + 2 * D + BN <= 512;
+  static constexpr uint32_t T_P0 = SEP_P ? 2 * BN + 2 * D : T_S0;
+  static constexpr uint32_t T_P1 = SEP_P ? 2 * BN + 2 * D + BN / 2 : T_S1;
   static_assert(SMEM <= 227 * 1024 - 512, "shared memory budget");
 };
 
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t q_full[L::QB], q_empty[L::QB], kv_full[L::NS], kv_empty[L::NS],
-      s_full[2], p_full[2][PCH], o_full[2], o_empty[2], q_rot[L::QB];
+      s_full[2], p_full[2][PCH], o_full[2], o_empty[2], q_rot[L::QB], s_free[2], pv_done[2];
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -245,6 +255,8 @@ __global__ void __launch_bounds__(384, 1)
       for (int q = 0; q < PCH; ++q) mbar_init(&p_full[g][q], 4);
       mbar_init(&o_full[g], 1);
       mbar_init(&o_empty[g], 4);
+      mbar_init(&s_free[g], 4);    // SEP_P: S columns read by the 4 softmax warps
+      mbar_init(&pv_done[g], 1);   // SEP_P: P.V of a tile complete (P buffer free)
     }
     fence_barrier_init();
   }
@@ -332,7 +344,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int k2 = 0; k2 < BN / 16 / PCH; ++k2) {
           const int kk = half * (BN / 16 / PCH) + k2;
-          mma_f16_ts(tmem + (g ? L::T_O1 : L::T_O0), tmem + (g ? L::T_S1 : L::T_S0) + kk * 8,
+          mma_f16_ts(tmem + (g ? L::T_O1 : L::T_O0), tmem + (g ? L::T_P1 : L::T_P0) + kk * 8,
                      umma_desc_sw128(v_addr + kk * 2048, L::CH, 1024), idesc_o,
                      !(first && kk == 0));
         }
@@ -351,6 +363,12 @@ __global__ void __launch_bounds__(384, 1)
           const uint32_t kseq = c + 2 * j, vseq = kseq + 1, knext = kseq + 2;
           // ---- query tile 0
           TRACE_MMA(j, 0)
+          if (L::SEP_P && more) {
+            // S_0 columns already read by the softmax: next S right away
+            mbar_wait(&s_free[0], t & 1);
+            wait_kv(knext);
+            issue_s(0, knext);
+          }
           mbar_wait(&p_full[0][0], t & 1);
           tc_fence_after();
           TRACE_MMA(j, 1)
@@ -367,15 +385,24 @@ __global__ void __launch_bounds__(384, 1)
             issue_pv(0, vseq, j == 0, q);
           }
           TRACE_MMA(j, 2)
+          if (L::SEP_P) mma_commit(&pv_done[0]);
           if (more) {
-            wait_kv(knext);
-            TRACE_MMA(j, 3)
-            issue_s(0, knext);
+            if (!L::SEP_P) {
+              wait_kv(knext);
+              TRACE_MMA(j, 3)
+              issue_s(0, knext);
+            }
           } else {
             mma_commit(&o_full[0]);
           }
           // ---- query tile 1
           TRACE_MMA(j, 4)
+          if (L::SEP_P && more) {
+            mbar_wait(&s_free[1], t & 1);
+            issue_s(1, knext);
+            mma_commit(&kv_empty[knext % L::NS]);
+            if (j + 2 == n_kv) mma_commit(&q_empty[qb]);
+          }
           mbar_wait(&p_full[1][0], t & 1);
           tc_fence_after();
           TRACE_MMA(j, 5)
@@ -391,10 +418,13 @@ __global__ void __launch_bounds__(384, 1)
             issue_pv(1, vseq, j == 0, q);
           }
           mma_commit(&kv_empty[vseq % L::NS]);
+          if (L::SEP_P) mma_commit(&pv_done[1]);
           if (more) {
-            issue_s(1, knext);
-            mma_commit(&kv_empty[knext % L::NS]);
-            if (j + 2 == n_kv) mma_commit(&q_empty[qb]);
+            if (!L::SEP_P) {
+              issue_s(1, knext);
+              mma_commit(&kv_empty[knext % L::NS]);
+              if (j + 2 == n_kv) mma_commit(&q_empty[qb]);
+            }
           } else {
             mma_commit(&o_full[1]);
           }
@@ -430,6 +460,7 @@ __global__ void __launch_bounds__(384, 1)
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t t_s = tmem + (g ? L::T_S1 : L::T_S0) + lane_off;
+    const uint32_t t_p = tmem + (g ? L::T_P1 : L::T_P0) + lane_off;
     const uint32_t t_o = tmem + (g ? L::T_O1 : L::T_O0) + lane_off;
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     uint32_t t = 0;
@@ -447,6 +478,12 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int ch = 0; ch < BN / 32; ++ch) tmem_ld_32x32b_x32(t_s + ch * 32, v + ch * 32);
         tmem_ld_wait();
+        if (L::SEP_P) {
+          // S is in registers: the MMA warp may write S_{j+1} now
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_free[g]);
+        }
         TRACE_SM(g, j, 2)
         if (kvalid < BN) {
 #pragma unroll
@@ -471,7 +508,12 @@ __global__ void __launch_bounds__(384, 1)
           alpha = ex2(m_used - m_new);
           if (j > 0) {
             // rescale the O row before any of P_j is released (O is current:
-            // S_{g,j} was issued after PV_{g,j-1})
+            // S_{g,j} was issued after PV_{g,j-1}; with a separate P buffer
+            // S_{g,j} may run ahead of it, so wait for that P.V)
+            if (L::SEP_P) {
+              mbar_wait(&pv_done[g], (t - 1) & 1);
+              tc_fence_after();
+            }
 #pragma unroll
             for (int ch = 0; ch < D / 32; ++ch) {
               uint32_t w[32];
@@ -486,6 +528,12 @@ __global__ void __launch_bounds__(384, 1)
         TRACE_SM(g, j, 3)
         const float2 nm2 = make_float2(-m_new, -m_new);
         float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        if (L::SEP_P && j > 0) {
+          // the P buffer is free once the previous tile's P.V completed
+          // (j = 0: the previous item's last P.V completed before o_full)
+          mbar_wait(&pv_done[g], (t - 1) & 1);
+          tc_fence_after();
+        }
 #pragma unroll
         for (int half = 0; half < PCH; ++half) {
 #pragma unroll
@@ -533,7 +581,7 @@ __global__ void __launch_bounds__(384, 1)
               pk[q] = pack2<BF16>(e.x, e.y);
             }
 #endif
-            tmem_st_32x32b_x16(t_s + ch * 16, pk);
+            tmem_st_32x32b_x16(t_p + ch * 16, pk);
           }
           // release this chunk of P_j to the MMA warp
           if (half == PCH - 1) { TRACE_SM(g, j, 6) }
