@@ -497,12 +497,14 @@ def test_add_beyond_int32_elements():
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("sq,sk", [(300, 700), (1000, 64), (129, 1)])
-def test_sdpa_cross_attention_lengths(sq, sk):
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("sq,sk", [(300, 700), (1000, 64), (129, 1), (256, 2000)])
+def test_sdpa_cross_attention_lengths(sq, sk, d):
     """S_q != S_k (cross attention): partial query tiles, partial and single-key
-    KV tiles, more KV tiles than query tiles and the reverse."""
-    rng = np.random.default_rng(sq * 7 + sk)
-    b, h, d = 2, 5, 128
+    KV tiles, more KV tiles than query tiles and the reverse; D = 64 runs the
+    separate-P-buffer schedule (S_{j+1} issued before P.V_j)."""
+    rng = np.random.default_rng(sq * 7 + sk + d)
+    b, h = 2, 5
     q = _r16(rng.uniform(-1, 1, (b, h, sq, d)).astype(np.float32), torch.float16)
     k = _r16(rng.uniform(-1, 1, (b, h, sk, d)).astype(np.float32), torch.float16)
     v = _r16(rng.uniform(-1, 1, (b, h, sk, d)).astype(np.float32), torch.float16)
