@@ -7,19 +7,20 @@
 //     B operand is split along N across the pair), O += P V with each CTA
 //     supplying 64 of the 128 head dims of a V tile.  Per SM that is half
 //     the K/V shared-memory traffic of the single-CTA kernel;
-//   * TMEM per CTA: two S buffers (S_j in buffer j & 1, P_j written in place
-//     into its first 64 columns) + O.  S_{j+1} is issued right after
-//     S_j, long before softmax_j ends, so the softmax runs tile after tile
-//     without waiting for P.V + S; S_{j+2} reuses buffer j & 1 after P.V_j
+//   * TMEM per CTA: NB = 3 S buffers (S_j in buffer j % 3, P_j written in
+//     place into its first 64 columns) + O.  S_{j+1} and S_{j+2} are issued
+//     long before softmax_j ends, so the softmax runs tile after tile
+//     without waiting for P.V + S; S_{j+3} reuses buffer j % 3 after P.V_j
 //     (in-order tensor pipe).  Two softmax warpgroups per CTA split each row
 //     (keys 0-63 / 64-127, O dims 0-63 / 64-127) and exchange the row max
 //     through shared memory once per tile;
 //   * warp 0: TMA producer (its CTA's Q tile and K / V halves; the bytes of
 //     both CTAs complete on CTA 0's barriers), warp 1 of CTA 0: the MMA
 //     issuer, warp 2: TMEM allocation, warps 4-11: softmax + epilogue.
-// Measured (B32 H32 S4096 D128): 7.51 ms vs 6.99 ms for the single-CTA v4
-// kernel (at higher clocks: 1570-1600 vs 1500 MHz), so it is NOT the
-// default; NTB_ATTN_PAIR=1 selects it for A/B runs.
+// Measured (B32 H32 S4096 D128): 7.5-7.8 ms vs 7.0-7.25 ms for the
+// single-CTA v4 kernel (at higher clocks: 1570-1600 vs 1485-1500 MHz); two
+// or three S buffers measure the same, so the wait for S is not what bounds
+// it.  NOT the default; NTB_ATTN_PAIR=1 selects it for A/B runs.
 //   * ring order K_0, K_1, {V_j, K_{j+2}}: exactly the order the MMAs
 //     release the slots in.
 // Softmax / lazy rescale / exp split as in v4.  P chunks, s_full and the
@@ -41,7 +42,12 @@ constexpr int Q_BYTES = BM * D * 2;            // 32 KB: this CTA's query tile
 constexpr int SLOT = 16384;                    // K half (64 keys x 128 d) or V half (128 keys x 64 d)
 constexpr int OFF_KV = Q_BYTES;
 constexpr int SMEM = OFF_KV + NS * SLOT + 1024;
-constexpr uint32_t T_S = 0, T_O = 2 * BN;      // S buffers [0,256), O [256,384)
+#ifndef NTB_PAIR_NB
+#define NTB_PAIR_NB 3
+#endif
+constexpr int NB = NTB_PAIR_NB;                // S buffers per CTA
+constexpr uint32_t T_S = 0, T_O = NB * BN;     // S buffers, then O
+static_assert(NB * BN + D <= 512, "TMEM budget");
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kThr = 8.0f;
 #ifndef NTB_ATTN_POLY_PAIRS
@@ -99,8 +105,9 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 // ring sequence (within an item of n tiles) of V_j and K_j
-__device__ __forceinline__ uint32_t seq_v(int j, int n) { return min(2 + 2 * j, 2 * n - 1); }
-__device__ __forceinline__ uint32_t seq_k(int j) { return j < 2 ? j : 2 * j - 1; }
+// ring order K_0 .. K_{NB-1}, then {V_j, K_{j+NB}}
+__device__ __forceinline__ uint32_t seq_v(int j, int n) { return min(NB + 2 * j, n + j); }
+__device__ __forceinline__ uint32_t seq_k(int j) { return j < NB ? j : 2 * j - NB + 1; }
 
 constexpr int THREADS = 384;   // warps 0-3 roles, 4-7 / 8-11 softmax halves
 
@@ -111,8 +118,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t q_full, q_empty, kv_full[NS], kv_empty[NS], s_full[2],
-      p_full[2][PCH], pv_done[2], o_full, o_empty;
+  __shared__ __align__(8) uint64_t q_full, q_empty, kv_full[NS], kv_empty[NS], s_full[NB],
+      p_full[NB][PCH], pv_done[NB], o_full, o_empty;
   __shared__ uint32_t tmem_slot;
   __shared__ float xmax[2][2][BM];   // [tile parity][half] row maxima
   __shared__ float xsum[2][BM];      // [half] row sums (epilogue)
@@ -129,7 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&pv_done[b], 1);
       for (int c = 0; c < PCH; ++c) mbar_init(&p_full[b][c], 8);   // 4 warps x 2 CTAs
@@ -179,11 +186,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                h, b);
           }
         };
-        load(c + 0, false, 0);
-        if (n_kv > 1) load(c + 1, false, 1);
+        for (int j = 0; j < NB && j < n_kv; ++j) load(c + j, false, j);
         for (int j = 0; j < n_kv; ++j) {
           load(c + seq_v(j, n_kv), true, j);
-          if (j + 2 < n_kv) load(c + seq_k(j + 2), false, j + 2);
+          if (j + NB < n_kv) load(c + seq_k(j + NB), false, j + NB);
         }
         c += 2 * n_kv;
       }
@@ -215,15 +221,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int item = cid; item < p.n_items; item += ncl, ++it) {
         mbar_wait(&q_full, it & 1);
         tc_fence_after();
-        wait_kv(c + 0);
-        issue_s(t & 1, c + 0);
-        if (n_kv > 1) {
-          wait_kv(c + 1);
-          issue_s((t + 1) & 1, c + 1);
+        for (int j = 0; j < NB && j < n_kv; ++j) {
+          wait_kv(c + j);
+          issue_s((t + j) % NB, c + j);
         }
-        if (n_kv <= 2) mma_commit_pair(&q_empty);
+        if (n_kv <= NB) mma_commit_pair(&q_empty);
         for (int j = 0; j < n_kv; ++j, ++t) {
-          const uint32_t buf = t & 1, ph = (t >> 1) & 1;
+          const uint32_t buf = t % NB, ph = (t / NB) & 1;
           const uint32_t vseq = c + seq_v(j, n_kv);
 #pragma unroll
           for (int q = 0; q < PCH; ++q) {
@@ -247,11 +251,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
           mma_commit_pair(&kv_empty[vseq % NS]);
           mma_commit_pair(&pv_done[buf]);
-          if (j + 2 < n_kv) {
-            const uint32_t kseq = c + seq_k(j + 2);
+          if (j + NB < n_kv) {
+            const uint32_t kseq = c + seq_k(j + NB);
             wait_kv(kseq);
             issue_s(buf, kseq);          // same buffer: after P.V_j in the pipe
-            if (j + 3 == n_kv) mma_commit_pair(&q_empty);
+            if (j + NB + 1 == n_kv) mma_commit_pair(&q_empty);
           }
           if (j + 1 == n_kv) mma_commit_pair(&o_full);
         }
@@ -275,9 +279,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const int qt = item % p.n_qt, bh = item / p.n_qt, h = bh % p.H, b = bh / p.H;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kv; ++j, ++t) {
-        const uint32_t buf = t & 1;
+        const uint32_t buf = t % NB, par = t & 1;
         const uint32_t t_s = tmem + T_S + buf * BN + lane_off;
-        mbar_wait(&s_full[buf], (t >> 1) & 1);
+        mbar_wait(&s_full[buf], (t / NB) & 1);
         tc_fence_after();
         const int kvalid = p.Sk - j * BN - hf * HB;
         uint32_t v[HB];
@@ -299,9 +303,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], __uint_as_float(v[i + u]));
         const float pmx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                 fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        xmax[buf][hf][row] = pmx;
+        xmax[par][hf][row] = pmx;
         asm volatile("bar.sync 1, 256;" ::: "memory");
-        const float mx = fmaxf(pmx, xmax[buf][hf ^ 1][row]);
+        const float mx = fmaxf(pmx, xmax[par][hf ^ 1][row]);
         const float cand = mx * p.scale_log2;
         const bool warp_grow = __any_sync(0xffffffffu, cand > m_used + kThr);
         float alpha = 1.f, m_new = m_used;
@@ -310,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           alpha = ex2(m_used - m_new);
           if (j > 0) {
             // S_j ran ahead of P.V_{j-1}: wait for it before touching O
-            mbar_wait(&pv_done[buf ^ 1], ((t - 1) >> 1) & 1);
+            mbar_wait(&pv_done[(t - 1) % NB], ((t - 1) / NB) & 1);
             tc_fence_after();
 #pragma unroll
             for (int ch = 0; ch < D / 64; ++ch) {
