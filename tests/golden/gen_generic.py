@@ -6,12 +6,15 @@ box); the output is committed:
 
     python tests/golden/gen_generic.py      # -> tests/golden/generic_cases.npz
 
-Three specs written directly in the reference's IR (tiledsl.tileir
+Specs written directly in the reference's IR (tiledsl.tileir
 KernelSpec / ArrangeOp / Reduce / BinOp, the `catalog._Builder` pattern,
 catalog.py:45-79), each exercising a reduction along ONE axis of a loaded
 tile - the broadcasting of the result follows tileir._broadcast
 (tileir.py:290-306) and sim.py:324-328 (numpy):
 
+* fma, gelu (x * sigmoid(1.702 x)), temp_softmax (exp(z - max z) / sum,
+  z = x / 2, on (1, BLOCK) rows), l2norm (x / sqrt(sum x^2 + 1e-6)): the
+  element-wise and whole-tile-reduction subset
 * rowsum    x (M, N) tiled (BM, BN) and squeezed to a 1-D grid, out (M,)
             tiled (BM,): out = sum(x, axis=1)
 * colexp    x, out (M, N) tiled (BM, BN): out = exp(x - max(x, axis=0))
@@ -38,8 +41,8 @@ def main():
     from tiledsl import sim
     from tiledsl.catalog import _Builder
     from tiledsl.symexpr import sym
-    from tiledsl.tileir import (BinOp, KernelSpec, Load, ParamSpec, Reduce, Store, UnOp,
-                                typecheck)
+    from tiledsl.tileir import (BinOp, ConstF, KernelSpec, Let, Load, Local, ParamSpec, Reduce,
+                                Store, UnOp, typecheck)
 
     BM, BN, B = sym("BM"), sym("BN"), sym("B")
 
@@ -72,7 +75,51 @@ def main():
             meta=("B",), arrangement={"a": tuple(a.ops), "c": tuple(c.ops)},
             application=(Store("c", BinOp("-", Load("a"), Reduce("sum", 1, Load("a")))),))
 
+    BLOCK = sym("BLOCK")
+
+    def fma():
+        bs = {n: _Builder(n, 1).tile((BLOCK,)) for n in ("x", "y", "z", "out")}
+        return KernelSpec(
+            name="fma", params=tuple(ParamSpec(n, 1, "f32", "out" if n == "out" else "in")
+                                     for n in ("x", "y", "z", "out")),
+            meta=("BLOCK",), arrangement={n: tuple(b.ops) for n, b in bs.items()},
+            application=(Store("out", BinOp("+", BinOp("*", Load("x"), Load("y")), Load("z"))),))
+
+    def gelu():
+        bs = {n: _Builder(n, 1).tile((BLOCK,)) for n in ("x", "out")}
+        return KernelSpec(
+            name="gelu", params=(ParamSpec("x", 1, "f32", "in"), ParamSpec("out", 1, "f32", "out")),
+            meta=("BLOCK",), arrangement={n: tuple(b.ops) for n, b in bs.items()},
+            application=(Store("out", BinOp("*", Load("x"), UnOp("sigmoid", BinOp(
+                "*", ConstF(1.702), Load("x"))))),))
+
+    def temp_softmax():
+        bs = {n: _Builder(n, 2).tile((1, BLOCK)) for n in ("x", "out")}
+        xl = Load("x", other=float("-inf"))
+        return KernelSpec(
+            name="temp_softmax",
+            params=(ParamSpec("x", 2, "f32", "in"), ParamSpec("out", 2, "f32", "out")),
+            meta=("BLOCK",), arrangement={n: tuple(b.ops) for n, b in bs.items()},
+            application=(
+                Let("z", BinOp("*", xl, ConstF(0.5))),
+                Let("e", UnOp("exp", BinOp("-", Local("z"), Reduce("max", 1, Local("z"))))),
+                Store("out", BinOp("/", Local("e"), Reduce("sum", 1, Local("e"))))))
+
+    def l2norm():
+        bs = {n: _Builder(n, 2).tile((1, BLOCK)) for n in ("x", "out")}
+        return KernelSpec(
+            name="l2norm",
+            params=(ParamSpec("x", 2, "f32", "in"), ParamSpec("out", 2, "f32", "out")),
+            meta=("BLOCK",), arrangement={n: tuple(b.ops) for n, b in bs.items()},
+            application=(Store("out", BinOp("/", Load("x"), UnOp("sqrt", BinOp(
+                "+", Reduce("sum", 1, BinOp("*", Load("x"), Load("x"))), ConstF(1e-6))))),))
+
     cases = [
+        ("fma", fma(), {"x": (5000,), "y": (5000,), "z": (5000,)}, {"out": (5000,)},
+         {"BLOCK": 1024}, 21),
+        ("gelu", gelu(), {"x": (777,)}, {"out": (777,)}, {"BLOCK": 256}, 22),
+        ("temp_softmax", temp_softmax(), {"x": (33, 1000)}, {"out": (33, 1000)}, {"BLOCK": 1024}, 23),
+        ("l2norm", l2norm(), {"x": (7, 4096)}, {"out": (7, 4096)}, {"BLOCK": 4096}, 24),
         ("rowsum", rowsum(), {"x": (100, 300)}, {"out": (100,)}, {"BM": 16, "BN": 512}, 11),
         ("colexp", colexp(), {"x": (100, 300)}, {"out": (100, 300)}, {"BM": 64, "BN": 32}, 12),
         ("rowcenter", rowcenter(), {"a": (40, 40)}, {"c": (40, 40)}, {"B": 16}, 13),

@@ -308,23 +308,31 @@ def test_generic_loop_local_on_b200():
 
 
 @pytest.mark.gpu
-def test_generic_axis_reductions_match_reference_sim():
-    """Pinned: the same three axis-reduction specs written in the reference's
-    own IR and run through the reference's sim.launch (fixtures from
-    tests/golden/gen_generic.py) against this package's make() kernels on the
-    generic path, fp32, within the reference's 1e-4 reduction tolerance
-    (verify.py:25)."""
+def test_generic_path_matches_reference_sim():
+    """Pinned: specs written in the reference's own IR and run through the
+    reference's sim.launch (fixtures from tests/golden/gen_generic.py) against
+    this package's make() kernels on the generic path, fp32, within the
+    reference's 1e-4 reduction tolerance (verify.py:25): element-wise (fma,
+    GELU approximation), whole-tile reductions (temperature softmax, l2-norm)
+    and axis reductions (row sums stored as a vector, exp(x - max(x, 0)),
+    a - sum(a, 1) broadcast along the last axis)."""
     import torch
     from pathlib import Path
 
     g = np.load(Path(__file__).resolve().parent / "golden" / "generic_cases.npz")
-    cases = [("rowsum", rowsum_kernel, "x", "out", {"BM": 16, "BN": 512}),
-             ("colexp", colnorm_kernel, "x", "out", {"BM": 64, "BN": 32}),
-             ("rowcenter", rowcenter_kernel, "a", "c", {"B": 16})]
-    for name, build, pin, pout, meta in cases:
-        x = torch.from_numpy(g[f"{name}.in.{pin}"]).cuda()
+    cases = [("fma", fma_kernel, ("x", "y", "z"), "out", {"BLOCK": 1024}),
+             ("gelu", gelu_kernel, ("x",), "out", {"BLOCK": 256}),
+             ("temp_softmax", temp_softmax_kernel, ("x",), "out", {"BLOCK": 1024}),
+             ("l2norm", l2norm_kernel, ("x",), "out", {"BLOCK": 4096}),
+             ("rowsum", rowsum_kernel, ("x",), "out", {"BM": 16, "BN": 512}),
+             ("colexp", colnorm_kernel, ("x",), "out", {"BM": 64, "BN": 32}),
+             ("rowcenter", rowcenter_kernel, ("a",), "c", {"B": 16})]
+    for name, build, pins, pout, meta in cases:
+        xs = [torch.from_numpy(g[f"{name}.in.{k}"]).cuda() for k in pins]
         ref = g[f"{name}.out.{pout}"]
         out = torch.zeros(ref.shape, device="cuda")
-        build()(x, out, **meta)
+        before = backend.path_counts()["jit"]
+        build()(*xs, out, **meta)
         torch.cuda.synchronize()
+        assert backend.path_counts()["jit"] == before + 1, name
         np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-4, atol=1e-5, err_msg=name)
