@@ -46,9 +46,6 @@ constexpr int BM = 128, BN = 128;  // query rows per tile, keys per KV tile
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
-#ifndef NTB_ATTN_STAGED
-#define NTB_ATTN_STAGED 1  // measured 7.18 vs 7.27 ms (B32 H32 S4096 D128)
-#endif
 #ifndef NTB_ATTN_POLY_PAIRS
 #define NTB_ATTN_POLY_PAIRS 4  // of every 16 score pairs, 2^x on the FMA pipe
 #endif
@@ -541,7 +538,6 @@ __global__ void __launch_bounds__(384, 1)
           for (int c2 = 0; c2 < BN / 32 / PCH; ++c2) {
             const int ch = half * (BN / 32 / PCH) + c2;
             uint32_t pk[16];
-#if NTB_ATTN_STAGED
             // staged: all 16 scale/subtract FFMA2, then all 2^x, then the
             // sums and packs - independent work laid out for the scheduler
             float2 xs[16], es[16];
@@ -565,23 +561,6 @@ __global__ void __launch_bounds__(384, 1)
               sum2[q & 1] = __fadd2_rn(sum2[q & 1], es[q]);
               pk[q] = pack2<BF16>(es[q].x, es[q].y);
             }
-#else
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const int i = ch * 32 + 2 * q;
-              const float2 x = __ffma2_rn(
-                  make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sc2, nm2);
-              float2 e;
-              if (((q * NTB_ATTN_POLY_PAIRS) % 16) < NTB_ATTN_POLY_PAIRS) {
-                e = ex2_poly2(x);
-              } else {
-                e.x = ex2(x.x);
-                e.y = ex2(x.y);
-              }
-              sum2[q & 1] = __fadd2_rn(sum2[q & 1], e);
-              pk[q] = pack2<BF16>(e.x, e.y);
-            }
-#endif
             tmem_st_32x32b_x16(t_p + ch * 16, pk);
           }
           // release this chunk of P_j to the MMA warp
