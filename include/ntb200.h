@@ -163,8 +163,10 @@ int ntb_jit_compile(const char* source, const char* kernel_name, int64_t* handle
 int ntb_jit_launch(int64_t handle, const int64_t* grid3, const int64_t* block3, void** args,
                    void* stream);
 
-/* Device scratch used by ntb_launch for strided-operand repacking; freed by
- * ntb_release_workspace (optional; the library frees it at unload).       */
+/* Device scratch used by ntb_launch (conv2d's repacked filter), kept per
+ * (device, stream).  A buffer used while a stream is captured into a CUDA
+ * graph stays allocated until this call, so calling it invalidates graphs
+ * captured over conv2d; re-capture them afterwards.                       */
 int ntb_release_workspace(void);
 
 #ifdef __cplusplus

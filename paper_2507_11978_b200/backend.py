@@ -117,25 +117,47 @@ def _canon_ir(node, ren, params, scope):
     return node
 
 
+def _node(n, *classes):
+    return isinstance(n, list) and n and isinstance(n[0], str) and n[0] in classes
+
+
+def _reads(n, acc):
+    """Names of the locals an ir_tree() expression reads."""
+    if _node(n, "Local"):
+        acc.add(dict(n[1:])["name"])
+    if isinstance(n, list):
+        for x in n:
+            _reads(x, acc)
+    return acc
+
+
+def _writes(n, acc):
+    """Names of the locals a statement (or block) Assigns / Accumulates."""
+    if _node(n, "Accumulate", "Assign"):
+        acc.add(dict(n[1:])["name"])
+    if isinstance(n, list):
+        for x in n:
+            _writes(x, acc)
+    return acc
+
+
 def _inline_lets(stmts):
-    """Inline every single-assignment local (Let never Accumulate'd or
-    Assign'ed) into its uses, on the ir_tree() form, so that equivalent
+    """Inline single-assignment locals (a Let whose name is never Accumulate'd
+    or Assign'ed) into their uses, on the ir_tree() form, so that equivalent
     formulations of the same application (e.g. the paper's softmax with its
-    `row_minus_max` temporaries vs the catalog's) compare equal."""
-    mutable = set()
+    `row_minus_max` temporaries vs the catalog's) compare equal.
 
-    def scan(n):
-        if isinstance(n, list) and n and isinstance(n[0], str) and n[0] in ("Accumulate", "Assign"):
-            mutable.add(dict(n[1:])["name"])
-        if isinstance(n, list):
-            for x in n:
-                scan(x)
-
-    scan(stmts)
+    A Let that reads a MUTABLE local is a snapshot: it is inlined only when
+    no write to that local can happen between the Let and any of its uses
+    (later in the same block, or anywhere in an enclosing loop body that
+    does not also contain the Let).  Otherwise it stays a Let, so a spec that
+    reads a frozen copy of a running value never fingerprints like one that
+    reads the live value."""
+    mutable = _writes(stmts, set())
     defs = {}
 
     def sub(n):
-        if isinstance(n, list) and n and n[0] == "Local":
+        if _node(n, "Local"):
             name = dict(n[1:])["name"]
             if name in defs:
                 return defs[name]
@@ -143,15 +165,37 @@ def _inline_lets(stmts):
             return [sub(x) for x in n]
         return n
 
+    def safe(name, deps, rest):
+        """rest: the statements after the Let in its block.  (A Let inside a
+        loop body re-snapshots every iteration, so only the rest of its own
+        block can put a write between it and a use.)"""
+        if not deps:
+            return True
+        written = set()
+        for st in rest:
+            if written & deps and name in _reads(st, set()):
+                return False
+            if _node(st, "ForRange"):
+                body = dict(st[1:])["body"]
+                if _writes(body, set()) & deps and name in _reads(body, set()):
+                    return False
+            written |= _writes(st, set())
+        return True
+
     def block(ss):
         out = []
-        for st in ss:
-            if isinstance(st, list) and st and st[0] == "Let":
+        for i, st in enumerate(ss):
+            if _node(st, "Let"):
                 f = dict(st[1:])
-                if f["name"] not in mutable:
-                    defs[f["name"]] = sub(f["expr"])
+                name = f["name"]
+                expr = sub(f["expr"])
+                if name not in mutable and safe(name, _reads(expr, set()) & mutable, ss[i + 1:]):
+                    defs[name] = expr
                     continue
-            if isinstance(st, list) and st and st[0] == "ForRange":
+                defs.pop(name, None)
+                out.append([st[0]] + [[k, expr if k == "expr" else v] for k, v in st[1:]])
+                continue
+            if _node(st, "ForRange"):
                 st = [st[0]] + [[k, block(v) if k == "body" else sub(v)] for k, v in st[1:]]
                 out.append(st)
                 continue

@@ -152,148 +152,200 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
 
 
-// ---- packed fp16 row math (issue-bound kernels: 2 elements per instruction) ----
-// max: HMNMX2 (exact); exp input (x - m) by HSUB2 (exact when x is within a
-// factor 2 of m - Sterbenz - otherwise one rounding of a value whose exp is
-// negligible), times log2e by HMUL2, exp2 on the SFU, e kept as fp16 in
-// place; row sum as fp16 partial sums of 8 values (each <= 1) accumulated
-// in fp32; normalisation by HMUL2.  rms_norm: squares of x * 2^-10 (no fp16
-// overflow for any finite fp16 x) summed 8 at a time, then fp32.  Error
-// <= a few fp16 ulp relative, inside the 1e-2 fp16 tolerance.  fp32 / bf16
-// rows keep the fp32 path.
-__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
-__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
-
-__device__ __forceinline__ void softmax_row_f16(const uint4* buf, __half* dst, int n_vec,
-                                                int lane) {
-  __half2 mx = __float2half2_rn(-INFINITY);
-  for (int c = lane; c < n_vec; c += 32) {
-    const uint4 v = buf[c];
-    mx = __hmax2(mx, __hmax2(__hmax2(u2h(v.x), u2h(v.y)), __hmax2(u2h(v.z), u2h(v.w))));
+// ---- 16-bit rows (fp16 / bf16): 16-bit I/O, fp32 arithmetic ----------------
+// The reference simulates every kernel in f32 (catalog.py:155-
+// 223).  Here every arithmetic operation is fp32: sm_100 has mixed-precision
+// FHADD / FHFMA (f32 result from f16 or bf16 register halves, PTX
+// add/sub/fma .f32.f16 / .f32.bf16), so a 16-bit element enters fp32 math
+// without a separate conversion.
+//   rms_norm: sum of x*x by FHFMA (each product exact in fp32, one rounding
+//     per accumulate: no scaling and no underflow for any 16-bit input);
+//     out = (x*w) * (1 / sqrt(ss / C + eps)): x*w is exact in fp32 (FHFMA
+//     with a zero addend), so the output carries one fp32 rounding + the
+//     store rounding.
+//   softmax: row max on the 16-bit pairs (HMNMX2, exact); d = x - m by FHADD
+//     (fp32), e = 2^(d log2 e) on the SFU (one ex2 per element), s = sum e
+//     in fp32.  e is held in the row's 16-bit type between the sum and the
+//     normalisation (the row stays register-resident: 64 registers a lane),
+//     so the output e * (1/s), computed in fp32, has two 16-bit roundings:
+//     <= 1 ulp of the output type (a single rounding would be 0.5 ulp).
+//     Recomputing e instead costs a second ex2 per element and made the
+//     kernel SFU-bound (14.4 vs 10.8 us at 4096 x 4096, B200).
+template <typename T> struct Pair16;
+template <> struct Pair16<__half> {
+  static __device__ __forceinline__ float2 f2(uint32_t u) {
+    return __half22float2(*reinterpret_cast<const __half2*>(&u));
   }
-  float m = fmaxf(__low2float(mx), __high2float(mx));
-  m = warp_max(m);
-  const __half2 l2e = __float2half2_rn(1.4426950408889634f);
-  const __half2 m2 = __float2half2_rn(m);   // exact: m is an fp16 value
-  float sum = 0.f;
-  uint4* ebuf = const_cast<uint4*>(buf);
-  for (int c = lane; c < n_vec; c += 32) {
-    const uint4 v = buf[c];
-    uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    __half2 acc = __float2half2_rn(0.f);
+  static __device__ __forceinline__ uint32_t pk(float2 f) {
+    const __half2 h = __float22half2_rn(f);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ uint32_t mx(uint32_t a, uint32_t b) {
+    const __half2 r = __hmax2(*reinterpret_cast<const __half2*>(&a),
+                              *reinterpret_cast<const __half2*>(&b));
+    return *reinterpret_cast<const uint32_t*>(&r);
+  }
+  // a + c and a * b + c with 16-bit a, b and fp32 c, d
+  static __device__ __forceinline__ float hadd(uint16_t a, float c) {
+    float d;
+    asm("add.f32.f16 %0, %1, %2;" : "=f"(d) : "h"(a), "f"(c));
+    return d;
+  }
+  static __device__ __forceinline__ float hfma(uint16_t a, uint16_t b, float c) {
+    float d;
+    asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+    return d;
+  }
+  static constexpr uint32_t kNegInf2 = 0xFC00FC00u;
+};
+template <> struct Pair16<__nv_bfloat16> {
+  static __device__ __forceinline__ float2 f2(uint32_t u) {
+    return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
+  }
+  static __device__ __forceinline__ uint32_t pk(float2 f) {
+    const __nv_bfloat162 h = __float22bfloat162_rn(f);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ uint32_t mx(uint32_t a, uint32_t b) {
+    const __nv_bfloat162 r = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&a),
+                                     *reinterpret_cast<const __nv_bfloat162*>(&b));
+    return *reinterpret_cast<const uint32_t*>(&r);
+  }
+  static __device__ __forceinline__ float hadd(uint16_t a, float c) {
+    float d;
+    asm("add.f32.bf16 %0, %1, %2;" : "=f"(d) : "h"(a), "f"(c));
+    return d;
+  }
+  static __device__ __forceinline__ float hfma(uint16_t a, uint16_t b, float c) {
+    float d;
+    asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+    return d;
+  }
+  static constexpr uint32_t kNegInf2 = 0xFF80FF80u;
+};
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t w4(const uint4& v, int k) {
+  return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ uint16_t lo16(uint32_t u) { return (uint16_t)(u & 0xFFFFu); }
+__device__ __forceinline__ uint16_t hi16(uint32_t u) { return (uint16_t)(u >> 16); }
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// Per-pack (8 elements) steps shared by the register-resident and the
+// shared-memory variants.
+template <typename T>
+struct Row16 {
+  using H = Pair16<T>;
+  static __device__ __forceinline__ uint32_t pack_max(uint32_t acc, const uint4& v) {
+    return H::mx(acc, H::mx(H::mx(v.x, v.y), H::mx(v.z, v.w)));
+  }
+  static __device__ __forceinline__ float pair_max(uint32_t p) {
+    const float2 f = H::f2(p);
+    return fmaxf(f.x, f.y);
+  }
+  // e = 2^((x - m) log2 e) of one pack, returned in T; acc += e (fp32)
+  static __device__ __forceinline__ uint4 exp_pack(const uint4& v, float nm, float2& acc) {
+    const float2 l2e = make_float2(kLog2e, kLog2e);
+    uint32_t o[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const __half2 x = __hmul2(__hsub2(u2h(w[k]), m2), l2e);
-      const __half2 e = h2exp2(x);
-      acc = __hadd2(acc, e);
-      w[k] = h2u(e);
+      const uint32_t u = w4(v, k);
+      const float2 t = __fmul2_rn(make_float2(H::hadd(lo16(u), nm), H::hadd(hi16(u), nm)), l2e);
+      const float2 e = make_float2(ex2f(t.x), ex2f(t.y));
+      acc = __fadd2_rn(acc, e);
+      o[k] = H::pk(e);
     }
-    const float2 a = __half22float2(acc);
-    sum += a.x + a.y;
-    ebuf[c] = make_uint4(w[0], w[1], w[2], w[3]);
+    return make_uint4(o[0], o[1], o[2], o[3]);
   }
-  const __half2 inv = __float2half2_rn(1.0f / warp_sum(sum));
-  for (int c = lane; c < n_vec; c += 32) {
-    const uint4 v = buf[c];
-    const uint4 o = make_uint4(h2u(__hmul2(u2h(v.x), inv)), h2u(__hmul2(u2h(v.y), inv)),
-                               h2u(__hmul2(u2h(v.z), inv)), h2u(__hmul2(u2h(v.w), inv)));
-    st_stream(dst + (int64_t)c * 8, o);
+  static __device__ __forceinline__ uint4 scale_pack(const uint4& e, float inv) {
+    const float2 i2 = make_float2(inv, inv);
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = H::pk(__fmul2_rn(H::f2(w4(e, k)), i2));
+    return make_uint4(o[0], o[1], o[2], o[3]);
   }
+  static __device__ __forceinline__ void sq_pack(const uint4& v, float (&acc)[4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t u = w4(v, k);
+      acc[k] = H::hfma(hi16(u), hi16(u), H::hfma(lo16(u), lo16(u), acc[k]));
+    }
+  }
+  static __device__ __forceinline__ uint4 rms_pack(const uint4& v, const uint4& g, float r) {
+    const float2 r2 = make_float2(r, r);
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t u = w4(v, k), q = w4(g, k);
+      const float2 xw = make_float2(H::hfma(lo16(u), lo16(q), 0.f), H::hfma(hi16(u), hi16(q), 0.f));
+      o[k] = H::pk(__fmul2_rn(xw, r2));
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  static __device__ __forceinline__ float rinv(const float (&acc)[4], int cols) {
+    const float ss = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+    return 1.0f / sqrtf(ss / (float)cols + kRmsEps);
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ void softmax_row16(const uint4* buf, T* dst, int n_vec, int lane) {
+  using R = Row16<T>;
+  uint32_t mx = Pair16<T>::kNegInf2;
+  for (int c = lane; c < n_vec; c += 32) mx = R::pack_max(mx, buf[c]);
+  const float nm = -warp_max(R::pair_max(mx));
+  float2 s2 = make_float2(0.f, 0.f);
+  uint4* ebuf = const_cast<uint4*>(buf);   // e overwrites the row in place
+  for (int c = lane; c < n_vec; c += 32) ebuf[c] = R::exp_pack(buf[c], nm, s2);
+  const float inv = 1.0f / warp_sum(s2.x + s2.y);
+  for (int c = lane; c < n_vec; c += 32) st_stream(dst + (int64_t)c * 8, R::scale_pack(buf[c], inv));
 }
 
-__device__ __forceinline__ void rms_row_f16(const uint4* buf, const uint4* wv, __half* dst,
-                                            int n_vec, int cols, int lane) {
-  float ss = 0.f;
-  const __half2 sc = __float2half2_rn(1.0f / 1024.0f);
-  for (int c = lane; c < n_vec; c += 32) {
-    const uint4 v = buf[c];
-    const __half2 a0 = __hmul2(u2h(v.x), sc), a1 = __hmul2(u2h(v.y), sc);
-    const __half2 a2 = __hmul2(u2h(v.z), sc), a3 = __hmul2(u2h(v.w), sc);
-    __half2 acc = __hmul2(a0, a0);
-    acc = __hfma2(a1, a1, acc);
-    acc = __hfma2(a2, a2, acc);
-    acc = __hfma2(a3, a3, acc);
-    const float2 a = __half22float2(acc);
-    ss += a.x + a.y;
-  }
-  ss *= 1048576.0f;   // undo the 2^-20 scaling of the squares
-  const float rinv = 1.0f / sqrtf(warp_sum(ss) / (float)cols + kRmsEps);
-  const __half2 r2 = __float2half2_rn(rinv);
-  for (int c = lane; c < n_vec; c += 32) {
-    const uint4 v = buf[c], g = wv[c];
-    const uint4 o = make_uint4(h2u(__hmul2(__hmul2(u2h(v.x), r2), u2h(g.x))),
-                               h2u(__hmul2(__hmul2(u2h(v.y), r2), u2h(g.y))),
-                               h2u(__hmul2(__hmul2(u2h(v.z), r2), u2h(g.z))),
-                               h2u(__hmul2(__hmul2(u2h(v.w), r2), u2h(g.w))));
-    st_stream(dst + (int64_t)c * 8, o);
-  }
+template <typename T>
+__device__ __forceinline__ void rms_row16(const uint4* buf, const uint4* wv, T* dst, int n_vec,
+                                          int cols, int lane) {
+  using R = Row16<T>;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int c = lane; c < n_vec; c += 32) R::sq_pack(buf[c], acc);
+  const float r = R::rinv(acc, cols);
+  for (int c = lane; c < n_vec; c += 32) st_stream(dst + (int64_t)c * 8, R::rms_pack(buf[c], wv[c], r));
 }
 
-// Register-resident variants for rows of exactly 32 * VPL packs (4096 fp16
-// columns = VPL 16): the row is read from shared memory ONCE into registers
-// (64 registers per lane) and the max / exp / sum / scale passes run there.
-template <int VPL>
-__device__ __forceinline__ void softmax_row_f16_reg(uint4 (&v)[VPL], __half* dst, int lane) {
-  __half2 mx = __float2half2_rn(-INFINITY);
+// Register-resident variants for rows of exactly 32 * VPL packs (4096
+// 16-bit columns = VPL 16): the row is read from shared memory ONCE into
+// registers (64 per lane) and every pass runs there.
+template <typename T, int VPL>
+__device__ __forceinline__ void softmax_row16_reg(uint4 (&v)[VPL], T* dst, int lane) {
+  using R = Row16<T>;
+  uint32_t mx = Pair16<T>::kNegInf2;
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) mx = R::pack_max(mx, v[u]);
+  const float nm = -warp_max(R::pair_max(mx));
+  float2 sa = make_float2(0.f, 0.f), sb = sa;
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) v[u] = R::exp_pack(v[u], nm, (u & 1) ? sb : sa);
+  const float inv = 1.0f / warp_sum((sa.x + sa.y) + (sb.x + sb.y));
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) st_stream(dst + (int64_t)(lane + 32 * u) * 8, R::scale_pack(v[u], inv));
+}
+
+template <typename T, int VPL>
+__device__ __forceinline__ void rms_row16_reg(const uint4 (&v)[VPL], const uint4* wv, T* dst,
+                                              int cols, int lane) {
+  using R = Row16<T>;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int u = 0; u < VPL; ++u) R::sq_pack(v[u], acc);
+  const float r = R::rinv(acc, cols);
 #pragma unroll
   for (int u = 0; u < VPL; ++u)
-    mx = __hmax2(mx, __hmax2(__hmax2(u2h(v[u].x), u2h(v[u].y)), __hmax2(u2h(v[u].z), u2h(v[u].w))));
-  float m = fmaxf(__low2float(mx), __high2float(mx));
-  m = warp_max(m);
-  const __half2 l2e = __float2half2_rn(1.4426950408889634f);
-  const __half2 m2 = __float2half2_rn(m);
-  float sum = 0.f;
-#pragma unroll
-  for (int u = 0; u < VPL; ++u) {
-    uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-    __half2 acc = __float2half2_rn(0.f);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const __half2 e = h2exp2(__hmul2(__hsub2(u2h(w[k]), m2), l2e));
-      acc = __hadd2(acc, e);
-      w[k] = h2u(e);
-    }
-    v[u] = make_uint4(w[0], w[1], w[2], w[3]);
-    const float2 a = __half22float2(acc);
-    sum += a.x + a.y;
-  }
-  const __half2 inv = __float2half2_rn(1.0f / warp_sum(sum));
-#pragma unroll
-  for (int u = 0; u < VPL; ++u) {
-    const uint4 o = make_uint4(h2u(__hmul2(u2h(v[u].x), inv)), h2u(__hmul2(u2h(v[u].y), inv)),
-                               h2u(__hmul2(u2h(v[u].z), inv)), h2u(__hmul2(u2h(v[u].w), inv)));
-    st_stream(dst + (int64_t)(lane + 32 * u) * 8, o);
-  }
-}
-
-template <int VPL>
-__device__ __forceinline__ void rms_row_f16_reg(uint4 (&v)[VPL], const uint4* wv, __half* dst,
-                                                int cols, int lane) {
-  float ss = 0.f;
-  const __half2 sc = __float2half2_rn(1.0f / 1024.0f);
-#pragma unroll
-  for (int u = 0; u < VPL; ++u) {
-    const __half2 a0 = __hmul2(u2h(v[u].x), sc), a1 = __hmul2(u2h(v[u].y), sc);
-    const __half2 a2 = __hmul2(u2h(v[u].z), sc), a3 = __hmul2(u2h(v[u].w), sc);
-    __half2 acc = __hmul2(a0, a0);
-    acc = __hfma2(a1, a1, acc);
-    acc = __hfma2(a2, a2, acc);
-    acc = __hfma2(a3, a3, acc);
-    const float2 a = __half22float2(acc);
-    ss += a.x + a.y;
-  }
-  ss *= 1048576.0f;
-  const float rinv = 1.0f / sqrtf(warp_sum(ss) / (float)cols + kRmsEps);
-  const __half2 r2 = __float2half2_rn(rinv);
-#pragma unroll
-  for (int u = 0; u < VPL; ++u) {
-    const uint4 g = wv[lane + 32 * u];
-    const uint4 o = make_uint4(h2u(__hmul2(__hmul2(u2h(v[u].x), r2), u2h(g.x))),
-                               h2u(__hmul2(__hmul2(u2h(v[u].y), r2), u2h(g.y))),
-                               h2u(__hmul2(__hmul2(u2h(v[u].z), r2), u2h(g.z))),
-                               h2u(__hmul2(__hmul2(u2h(v[u].w), r2), u2h(g.w))));
-    st_stream(dst + (int64_t)(lane + 32 * u) * 8, o);
-  }
+    st_stream(dst + (int64_t)(lane + 32 * u) * 8, R::rms_pack(v[u], wv[lane + 32 * u], r));
 }
 
 template <typename T, bool kSoftmax>
@@ -360,7 +412,7 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
         }
       }
     };
-    if constexpr (std::is_same<T, __half>::value) {
+    if constexpr (sizeof(T) == 2) {
       if (n_vec == 32 * 16 && NTB_ROWS_REG) {
         // the row moves to registers and the next row's copy starts before
         // any of this row's math or stores
@@ -368,19 +420,18 @@ __global__ void __launch_bounds__(kStreamWarps * 32, 1)
 #pragma unroll
         for (int u = 0; u < 16; ++u) v[u] = buf[lane + 32 * u];
         refill();
-        if (kSoftmax) softmax_row_f16_reg<16>(v, dst, lane);
-        else rms_row_f16_reg<16>(v, reinterpret_cast<const uint4*>(wsh), dst, cols, lane);
+        if (kSoftmax) softmax_row16_reg<T, 16>(v, dst, lane);
+        else rms_row16_reg<T, 16>(v, reinterpret_cast<const uint4*>(wsh), dst, cols, lane);
         continue;
       } else if (kSoftmax) {
-        softmax_row_f16(buf, dst, n_vec, lane);
+        softmax_row16<T>(buf, dst, n_vec, lane);
       } else {
-        rms_row_f16(buf, reinterpret_cast<const uint4*>(wsh), dst, n_vec, cols, lane);
+        rms_row16<T>(buf, reinterpret_cast<const uint4*>(wsh), dst, n_vec, cols, lane);
       }
     } else if (kSoftmax) {
-      // pass 1: row max; pass 2: e = exp(x - m) written back in place (fp16
-      // for 16-bit rows, fp32 for fp32 rows) + row sum; pass 3: e / sum.
-      // One exponential per element (the SFU, not HBM, would otherwise bound).
-      using E = typename std::conditional<sizeof(T) == 4, float, __half>::type;
+      // fp32 rows. pass 1: row max; pass 2: e = exp(x - m) written back in
+      // place (fp32, exact) + row sum; pass 3: e / sum.
+      using E = float;
       float m = -INFINITY;
       for (int c = lane; c < n_vec; c += 32) {
         P v;

@@ -179,7 +179,7 @@ NTB_HD int eval_point(const Blob& B, int q, int64_t linear, const int64_t* nest_
     if (rc) return rc;
     rc = eval_code(m.mask_bound[i].code, m.mask_bound[i].len, slots, B.n_slots, &bnd);
     if (rc) return rc;
-    ok = ok && (l < bnd);
+    ok = ok && l >= 0 && l < bnd;   // sim.py _offsets_and_mask: (lhs >= 0) & (lhs < bound)
   }
   *mask = ok;
   return 0;

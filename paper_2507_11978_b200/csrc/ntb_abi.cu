@@ -6,6 +6,7 @@
 #include <atomic>
 #include <mutex>
 #include <map>
+#include <vector>
 #include <utility>
 #include <string>
 
@@ -51,18 +52,26 @@ int sm_count() {
   return cached[dev];
 }
 
-// Library-owned scratch (conv's repacked filter + image, sdpa_rope's rotated
-// K) is kept PER STREAM: within a stream, reuse is ordered by the stream;
-// two streams never share a buffer (except inside a CUDA-graph capture, see
-// below).  Growth frees the old buffer after a
-// device-wide sync (cudaFree), so no in-flight kernel still reads it.
+// Library-owned scratch (conv's repacked filter) is kept PER STREAM: within a
+// stream, reuse is ordered by the stream; two streams never share a buffer.
+// Eager growth frees the old buffer after a sync of its stream.  A buffer
+// handed out while the stream is being CAPTURED into a CUDA graph is baked
+// into that graph, so it is "pinned": it is never freed on growth (only
+// retired, still allocated) and lives until ntb_release_workspace(), which
+// therefore invalidates any graph captured over a workspace-using kernel.
+// Growth during a capture allocates a fresh buffer (in relaxed capture mode
+// for this thread: cudaMalloc is not a stream operation) instead of handing
+// out another stream's buffer.  Graphs captured on the same stream share its
+// buffer: replay them in order on one stream, not concurrently.
 struct Ws {
   void* p = nullptr;
   size_t bytes = 0;
+  bool pinned = false;
 };
 static std::mutex g_ws_mu;
 // keyed by (device, stream): the legacy default stream is per device
 static std::map<std::pair<int, cudaStream_t>, Ws> g_ws;
+static std::vector<std::pair<int, void*>> g_ws_retired;
 
 void* workspace(size_t bytes, cudaStream_t s) {
   int dev = 0;
@@ -70,33 +79,38 @@ void* workspace(size_t bytes, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cap);
-  if (cap != cudaStreamCaptureStatusNone) {
-    // CUDA-graph capture (often on a side stream): no allocation or sync is
-    // legal here, so the graph bakes in this device's largest workspace -
-    // run the op once outside capture first (warm-up) to size it
-    auto it = g_ws.find({dev, s});
-    if (it != g_ws.end() && it->second.bytes >= bytes) return it->second.p;
-    Ws* best = nullptr;
-    for (auto& kv : g_ws)
-      if (kv.first.first == dev && kv.second.bytes >= bytes &&
-          (!best || kv.second.bytes > best->bytes))
-        best = &kv.second;
-    return best ? best->p : nullptr;
-  }
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
   Ws& w = g_ws[{dev, s}];
-  if (bytes > w.bytes) {
-    if (w.p) {
+  if (bytes <= w.bytes) {
+    w.pinned = w.pinned || capturing;
+    return w.p;
+  }
+  if (w.p) {
+    if (w.pinned || capturing) {
+      g_ws_retired.emplace_back(dev, w.p);   // a graph (or in-flight work) may hold it
+    } else {
       cudaStreamSynchronize(s);
       cudaFree(w.p);
     }
-    w.p = nullptr;
-    w.bytes = 0;
-    if (cudaMalloc(&w.p, bytes) != cudaSuccess) {
-      w.p = nullptr;
-      return nullptr;
-    }
-    w.bytes = bytes;
   }
+  w = Ws{};
+  void* p = nullptr;
+  cudaError_t e;
+  if (capturing) {
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    e = cudaMalloc(&p, bytes);
+    cudaThreadExchangeStreamCaptureMode(&mode);
+  } else {
+    e = cudaMalloc(&p, bytes);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  w.p = p;
+  w.bytes = bytes;
+  w.pinned = capturing;
   return w.p;
 }
 
@@ -346,8 +360,13 @@ int ntb_release_workspace(void) {
       cudaSetDevice(kv.first.first);
       cudaFree(kv.second.p);
     }
+  for (auto& r : g_ws_retired) {
+    cudaSetDevice(r.first);
+    cudaFree(r.second);
+  }
   cudaSetDevice(cur);
   g_ws.clear();
+  g_ws_retired.clear();
   return NTB_OK;
 }
 

@@ -38,11 +38,8 @@ struct Nvrtc {
   bool ok = false;
 };
 
-Nvrtc* nvrtc() {
+static Nvrtc* nvrtc_load() {
   static Nvrtc n;
-  static bool tried = false;
-  if (tried) return n.ok ? &n : nullptr;
-  tried = true;
   const char* names[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"};
   void* h = nullptr;
   for (const char* nm : names)
@@ -67,11 +64,8 @@ struct Driver {
   bool ok = false;
 };
 
-Driver* driver() {
+static Driver* driver_load() {
   static Driver d;
-  static bool tried = false;
-  if (tried) return d.ok ? &d : nullptr;
-  tried = true;
   cudaDriverEntryPointQueryResult q;
   void* p = nullptr;
   if (cudaGetDriverEntryPoint("cuModuleLoadData", &p, cudaEnableDefault, &q) == cudaSuccess && p)
@@ -84,6 +78,18 @@ Driver* driver() {
     d.launch = (decltype(d.launch))p;
   d.ok = d.load && d.getfn && d.launch;
   return d.ok ? &d : nullptr;
+}
+
+// Function-local statics are initialised exactly once (thread-safe under
+// C++11), so two threads doing their first compile never see a half-filled
+// table.
+Nvrtc* nvrtc() {
+  static Nvrtc* const n = nvrtc_load();
+  return n;
+}
+Driver* driver() {
+  static Driver* const d = driver_load();
+  return d;
 }
 
 std::mutex g_mu;

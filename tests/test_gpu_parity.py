@@ -171,6 +171,32 @@ def test_rows_fp16_large_magnitudes(scale):
     _close(got, oracle.rms_norm(x, w), rtol=1e-2, atol=1e-2)
 
 
+@pytest.mark.parametrize("dtype", DTS)
+@pytest.mark.parametrize("cols", [4096, 1000, 8192])
+@pytest.mark.parametrize("std", [0.01, 0.05, 0.1, 0.3, 1.0, 100.0])
+def test_rows_magnitude_sweep(dtype, cols, std):
+    """16-bit rows are computed in fp32 (the reference simulates in f32,
+    catalog.py:155-223): the only 16-bit rounding is the store,
+    so the result must sit within ~one output ulp of the f32 oracle at EVERY
+    activation scale, small ones included (sum of squares of N(0, 0.01^2)
+    must not underflow), plus an all-zero row (softmax -> 1/C, rms -> 0).
+    Tolerance: rtol = 2 ulp of the 16-bit type (fp16 2^-9, bf16 2^-6) and an
+    atol at the type's subnormal spacing."""
+    rng = np.random.default_rng(int(std * 1000) + cols)
+    x = (rng.standard_normal((96, cols)) * std).astype(np.float32)
+    x[5] = 0.0
+    x = _r16(x, dtype)
+    w = _r16(rng.uniform(-1, 1, cols).astype(np.float32), dtype)
+    rtol = 2.0 ** -9 if dtype == torch.float16 else 2.0 ** -6
+    atol = 1e-7 if dtype == torch.float16 else 1e-30
+    got = _run("softmax", {"input": x}, {"COLS_PADDED": cols}, dtype)
+    _close(got, oracle.softmax(x, cols).astype(np.float64), rtol=rtol, atol=atol)
+    np.testing.assert_allclose(got[5].float().cpu().numpy(), 1.0 / cols, rtol=rtol)
+    got = _run("rms_norm", {"input": x, "weight": w}, {"COLS_PADDED": cols}, dtype)
+    _close(got, oracle.rms_norm(x, w).astype(np.float64), rtol=rtol, atol=atol)
+    assert not got[5].any()
+
+
 def test_softmax_chunked_matches_reference_semantics():
     rng = np.random.default_rng(1)
     x = rng.uniform(-1, 1, (3, 20)).astype(np.float32)
@@ -665,18 +691,29 @@ def test_workspace_is_per_stream():
         torch.cuda.synchronize()
         for (args, _fn), ref in zip(cases, expect):
             assert torch.equal(args[-1], ref)
-    # CUDA-graph capture (torch captures on a side stream): after the warm-up
-    # above, the captured ops reuse the device's workspace without allocating
+    # CUDA-graph capture on a fresh stream (no buffer yet: the capture
+    # allocates its own, pinned), then an eager call on the SAME stream that
+    # grows the workspace: the graph's buffer must stay alive (retired, not
+    # freed) and the replay must still be exact (ntb_abi.cu).
+    cap = torch.cuda.Stream()
     graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
+    with torch.cuda.graph(graph, stream=cap):
         for args, fn in cases:
             fn(args)
-    for args, _fn in cases:
-        args[-1].fill_(float("nan"))
-    graph.replay()
+    xb, wb = U(2, 256, 20, 20), U(256, 256, 3, 3)
+    yb = torch.empty((2, 256, 18, 18), device=DEV, dtype=f16)
+    with torch.cuda.stream(cap):
+        backend.conv2d_launch(xb, wb, yb, 128, 128, 64)
     torch.cuda.synchronize()
-    for (args, _fn), ref in zip(cases, expect):
-        assert torch.equal(args[-1], ref)
+    for _ in range(2):
+        for args, _fn in cases:
+            args[-1].fill_(float("nan"))
+        graph.replay()
+        torch.cuda.synchronize()
+        for (args, _fn), ref in zip(cases, expect):
+            assert torch.equal(args[-1], ref)
+    ref = torch.nn.functional.conv2d(xb.float(), wb.float())
+    assert (yb.float() - ref).abs().max().item() < 0.5
 
 
 @pytest.mark.parametrize("shape", [("1", "2", "256", "128"), ("2", "3", "1000", "128")])

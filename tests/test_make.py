@@ -123,3 +123,33 @@ def test_make_kernels_run_on_b200():
     Y = torch.empty_like(X)
     softmax_kernel()(X, Y, BLOCK_SIZE=1024)
     torch.testing.assert_close(Y.float(), torch.softmax(X.float(), 1), rtol=1e-2, atol=1e-4)
+
+
+def test_snapshot_of_a_running_value_is_not_the_live_value():
+    """A Let that snapshots a mutable local before the loop (m0 = m) and is
+    read inside the loop must NOT be inlined into the live m: the variant
+    computes something else than attention and must not resolve to the
+    native sdpa family (backend._inline_lets)."""
+    import dataclasses
+
+    from paper_2507_11978_b200 import catalog as C
+    from paper_2507_11978_b200.spec import BinOp, ForRange, Let, Local, typecheck
+
+    spec = C.catalog("sdpa")
+    assert backend._family_of(typecheck(spec)) == "sdpa"
+    app = list(spec.application)
+    loop_at = next(i for i, st in enumerate(app) if isinstance(st, ForRange))
+    loop = app[loop_at]
+
+    def freeze(node):
+        # m_new = max(m0, rowmax(s)) instead of max(m, rowmax(s))
+        if isinstance(node, Let) and node.name == "m_new":
+            assert isinstance(node.expr, BinOp) and node.expr.a == Local("m")
+            return dataclasses.replace(node, expr=dataclasses.replace(node.expr, a=Local("m0")))
+        return node
+
+    frozen = dataclasses.replace(loop, body=tuple(freeze(st) for st in loop.body))
+    app[loop_at:loop_at + 1] = [Let("m0", Local("m")), frozen]
+    variant = dataclasses.replace(spec, application=tuple(app))
+    with pytest.raises(backend.UnsupportedSpecError):
+        backend._family_of(typecheck(variant))
