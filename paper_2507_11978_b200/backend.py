@@ -206,9 +206,14 @@ def _inline_lets(stmts):
 
 
 def _fingerprint(checked):
-    """Structural identity of a CheckedSpec - grid, checks, maps, IR - with
-    parameter, meta, local and kernel names factored out, so that any spec
-    that computes the same thing (e.g. one written through make()) matches."""
+    """Identity of a CheckedSpec - grid, checks, maps, IR - with parameter,
+    meta, local and kernel names factored out, so that any spec that
+    computes the same thing (e.g. one written through make()) matches.
+    Integer maps are compared by their canonical form (symbolic.canonical:
+    polynomial normal form over floor-div / mod atoms), so the front end
+    that built them - this package's, the reference's, a user's - and the
+    order it built them in do not matter; launch checks are compared as an
+    orientation-free set."""
     spec = checked.spec
     ren, params = {}, {}
     for i, p in enumerate(spec.params):
@@ -220,7 +225,7 @@ def _fingerprint(checked):
         ren[m] = f"m{j}"
 
     def tr(e):
-        return repr(_rename_tree(se.to_tree(se.from_any(e)), ren))
+        return se.canonical(se.from_tree(_rename_tree(se.to_tree(se.from_any(e)), ren)))
 
     maps = []
     for p in spec.params:
@@ -238,7 +243,7 @@ def _fingerprint(checked):
         tuple((p.rank, p.role) for p in spec.params),
         len(spec.meta),
         tuple(tr(s) for s in checked.grid.sizes),
-        tuple((tr(a), tr(b)) for a, b in checked.grid.checks),
+        frozenset(frozenset((tr(a), tr(b))) for a, b in checked.grid.checks),
         tuple(maps),
         repr(_canon_ir(_inline_lets(ir_tree(spec.application)), ren, params, {})),
     )

@@ -105,34 +105,47 @@ class Manifest:
     launcher_args: tuple
 
 
+def _manifest_problems(m: Manifest) -> list:
+    """Everything wrong with a parsed manifest, so one error reports all."""
+    problems = []
+    for p in m.params:
+        if p.kind not in KINDS:
+            problems.append(f"{p.name}: element kind {p.kind!r} is not one of {'/'.join(KINDS)}")
+        if p.role not in ROLES:
+            problems.append(f"{p.name}: role {p.role!r} is neither 'in' nor 'out'")
+        if p.rank < 0:
+            problems.append(f"{p.name}: rank {p.rank} < 0")
+    order = tuple(p.name for p in m.params) + m.meta
+    if m.launcher_args != order:
+        problems.append(f"launcher argument order {list(m.launcher_args)} is not parameters "
+                        f"then meta {list(order)}")
+    n_out = sum(p.role == "out" for p in m.params)
+    if n_out != 1:
+        problems.append(f"{n_out} output parameters; the runner compares exactly one")
+    return problems
+
+
 def load_manifest(path) -> Manifest:
+    """Parse and validate the sidecar that `tiledsl emit` writes next to a
+    kernel (the reference's emit.py:296-308 schema)."""
     path = Path(path)
     try:
         doc = json.loads(path.read_bytes())
+        if not isinstance(doc, dict):
+            raise TypeError("top level is not an object")
+        m = Manifest(
+            name=str(doc["name"]),
+            params=tuple(Param(str(e["name"]), int(e["rank"]), str(e["kind"]), str(e["role"]))
+                         for e in doc["params"]),
+            meta=tuple(map(str, doc["meta"])),
+            launcher_args=tuple(map(str, doc["launcher_args"])))
     except OSError as exc:
-        raise ManifestError(f"cannot read manifest {path}: {exc}") from exc
-    except ValueError as exc:
-        raise ManifestError(f"{path}: invalid JSON: {exc}") from exc
-    if not isinstance(doc, dict):
-        raise ManifestError(f"{path}: manifest must be a JSON object")
-    try:
-        params = tuple(Param(str(p["name"]), int(p["rank"]), str(p["kind"]), str(p["role"]))
-                       for p in doc["params"])
-        m = Manifest(str(doc["name"]), params, tuple(str(x) for x in doc["meta"]),
-                     tuple(str(x) for x in doc["launcher_args"]))
-    except (KeyError, TypeError, ValueError) as exc:
-        raise ManifestError(f"{path}: malformed manifest: {exc}") from exc
-    for p in m.params:
-        if p.kind not in KINDS:
-            raise ManifestError(f"{path}: param {p.name!r} has unknown kind {p.kind!r}")
-        if p.role not in ROLES:
-            raise ManifestError(f"{path}: param {p.name!r} has unknown role {p.role!r}")
-        if p.rank < 0:
-            raise ManifestError(f"{path}: param {p.name!r} has negative rank")
-    if m.launcher_args != tuple(p.name for p in m.params) + m.meta:
-        raise ManifestError(f"{path}: launcher_args do not match params + meta")
-    if sum(p.role == "out" for p in m.params) != 1:
-        raise ManifestError(f"{path}: expected exactly one output param")
+        raise ManifestError(f"manifest {path} unreadable: {exc}") from exc
+    except (ValueError, KeyError, TypeError) as exc:
+        raise ManifestError(f"manifest {path} is not a kernel manifest ({exc})") from exc
+    problems = _manifest_problems(m)
+    if problems:
+        raise ManifestError(f"manifest {path}: " + "; ".join(problems))
     return m
 
 
@@ -158,41 +171,38 @@ class Report:
     details: dict = field(default_factory=dict)
 
 
+def _as_param_array(arr: np.ndarray, p: Param) -> np.ndarray:
+    # `tiledsl simulate --save-dir` writes rank-0 scalars (addmm beta / alpha)
+    # through np.ascontiguousarray, i.e. with shape (1,) (tensorio.py:25-36,
+    # cli.py:217-222): a one-element file feeds a rank-0 parameter
+    return arr.reshape(()) if p.rank == 0 and arr.size == 1 else arr
+
+
 def build_request(manifest_path, input_paths: dict, expect_path, meta: dict, tol=None,
                   source=None) -> Request:
+    """Load every artifact and check it against the manifest; all problems
+    with names (inputs, meta) are reported together."""
     if source is not None and not Path(source).is_file():
-        raise ManifestError(f"kernel source not found: {source}")
+        raise ManifestError(f"--source {source} does not exist")
     m = load_manifest(manifest_path)
     ins = {p.name: p for p in m.params if p.role == "in"}
-    out = next(p for p in m.params if p.role == "out")
-    missing = sorted(set(ins) - set(input_paths))
-    if missing:
-        raise ManifestError(f"missing input tensors for params: {', '.join(missing)}")
-    extra = sorted(set(input_paths) - set(ins))
-    if extra:
-        raise ManifestError(f"unknown input params: {', '.join(extra)}")
-    inputs = {}
-    for name, path in input_paths.items():
-        arr = read_tensor(path)
-        if ins[name].rank == 0 and arr.size == 1:
-            # `tiledsl simulate --save-dir` writes rank-0 scalars (addmm beta /
-            # alpha) through np.ascontiguousarray, i.e. as shape (1,)
-            # (tensorio.py:25-36, cli.py:217-222); accept them as scalars.
-            arr = arr.reshape(())
-        if arr.ndim != ins[name].rank:
-            raise ManifestError(f"input {name!r}: file {path} has rank {arr.ndim}, "
-                                f"manifest says {ins[name].rank}")
-        inputs[name] = arr
+    problems = [f"no tensor file for input {n!r}" for n in sorted(set(ins) - set(input_paths))]
+    problems += [f"{n!r} is not an input of {m.name}" for n in sorted(set(input_paths) - set(ins))]
+    problems += [f"no value for meta {n}" for n in sorted(set(m.meta) - set(meta))]
+    problems += [f"{n} is not a meta-parameter of {m.name}" for n in sorted(set(meta) - set(m.meta))]
+    problems += [f"meta {n}={v} is not positive" for n, v in sorted(meta.items()) if v <= 0]
+    if problems:
+        raise ManifestError("; ".join(problems))
+    inputs = {n: _as_param_array(read_tensor(path), ins[n]) for n, path in input_paths.items()}
+    wrong = [f"{n}: {path} holds a rank-{inputs[n].ndim} tensor, {m.name} takes rank "
+             f"{ins[n].rank}" for n, path in input_paths.items() if inputs[n].ndim != ins[n].rank]
     expected = read_tensor(expect_path)
+    out = next(p for p in m.params if p.role == "out")
     if expected.ndim != out.rank:
-        raise ManifestError(f"expected output has rank {expected.ndim}, manifest says {out.rank}")
-    if sorted(set(m.meta) - set(meta)):
-        raise ManifestError(f"missing meta values: {', '.join(sorted(set(m.meta) - set(meta)))}")
-    if sorted(set(meta) - set(m.meta)):
-        raise ManifestError(f"unknown meta values: {', '.join(sorted(set(meta) - set(m.meta)))}")
-    for k, v in meta.items():
-        if v <= 0:
-            raise ManifestError(f"meta {k} must be a positive integer, got {v}")
+        wrong.append(f"expected output {expect_path} is rank {expected.ndim}, {out.name} is rank "
+                     f"{out.rank}")
+    if wrong:
+        raise ManifestError("; ".join(wrong))
     return Request(m, inputs, expected, dict(meta),
                    default_tolerance(m) if tol is None else float(tol))
 

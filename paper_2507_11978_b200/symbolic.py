@@ -390,3 +390,134 @@ def text(e, cdiv: str = "cdiv", fmin: str = "min", fmax: str = "max") -> str:
         return f"({s})" if p < parent else s
 
     return r(lift(e).node, 0)
+
+
+# --- canonical form (structural comparison up to algebra) -------------------
+#
+# Two front ends can build the same map with different association /
+# commutation orders (a*(b*c) vs (b*a)*c, x + 0, ...).  ``canonical`` turns an
+# expression into a hashable normal form: a polynomial with integer
+# coefficients over ATOMS, where an atom is a symbol or a floordiv / ceildiv /
+# mod / min / max of two canonical operands.  On top of ring arithmetic it
+# applies the exact identities (q*c) // c = q, (q*c) % c = 0 (c a constant
+# or a monomial dividing every term; c != 0), x // 1 = x, x % 1 = 0, and
+# (x // b) // c = x // (b*c), which assumes positive divisors - true for
+# every divisor an arrangement produces (tile sizes and extents).  Equal
+# canonical forms imply equal values under every binding with positive
+# divisors; the converse is not claimed (the backend only needs "same form
+# => same map", and tests check the forms of both front ends agree).
+
+def _padd(p, q, sign=1):
+    out = dict(p)
+    for m, c in q.items():
+        v = out.get(m, 0) + sign * c
+        if v:
+            out[m] = v
+        else:
+            out.pop(m, None)
+    return out
+
+
+def _pmul(p, q):
+    out: dict = {}
+    for m1, c1 in p.items():
+        for m2, c2 in q.items():
+            m = tuple(sorted(m1 + m2))
+            v = out.get(m, 0) + c1 * c2
+            if v:
+                out[m] = v
+            else:
+                out.pop(m, None)
+    return out
+
+
+def _pkey(p):
+    return tuple(sorted(p.items()))
+
+
+def _pconst(p):
+    if not p:
+        return 0
+    if len(p) == 1 and () in p:
+        return p[()]
+    return None
+
+
+def _atom(kind, pa, pb):
+    return {((kind, _pkey(pa), _pkey(pb)),): 1}
+
+
+def _divide_by_monomial(p, mono):
+    """p / mono if mono divides every monomial of p (multiset inclusion)."""
+    out = {}
+    for m, c in p.items():
+        rest = list(m)
+        for a in mono:
+            if a not in rest:
+                return None
+            rest.remove(a)
+        out[tuple(rest)] = c
+    return out
+
+
+def _poly(n):
+    k = n[0]
+    if k == "const":
+        return {(): n[1]} if n[1] else {}
+    if k == "sym":
+        return {(("sym", n[1]),): 1}
+    if k == "neg":
+        return {m: -c for m, c in _poly(n[1]).items()}
+    pa, pb = _poly(n[1]), _poly(n[2])
+    if k == "add":
+        return _padd(pa, pb)
+    if k == "sub":
+        return _padd(pa, pb, -1)
+    if k == "mul":
+        return _pmul(pa, pb)
+    if k in ("min", "max"):
+        ka, kb = _pkey(pa), _pkey(pb)
+        if ka == kb:
+            return pa
+        ca, cb = _pconst(pa), _pconst(pb)
+        if ca is not None and cb is not None:
+            v = min(ca, cb) if k == "min" else max(ca, cb)
+            return {(): v} if v else {}
+        lo, hi = sorted((ka, kb))
+        return {((k, lo, hi),): 1}
+    # floordiv / ceildiv / mod
+    ca, cb = _pconst(pa), _pconst(pb)
+    if cb is not None and cb != 0:
+        if ca is not None:
+            v = int(evaluate(Expr((k, ("const", ca), ("const", cb))), {}))
+            return {(): v} if v else {}
+        if all(c % cb == 0 for c in pa.values()):
+            return {} if k == "mod" else {m: c // cb for m, c in pa.items()}
+    elif cb is None and len(pb) == 1:
+        (mono, coeff), = pb.items()
+        if coeff == 1:
+            q = _divide_by_monomial(pa, mono)
+            if q is not None:
+                return {} if k == "mod" else q
+    if not pa and (cb is None or cb != 0):
+        return {}
+    if k == "floordiv" and len(pa) == 1:
+        (mono, coeff), = pa.items()
+        if coeff == 1 and len(mono) == 1 and mono[0][0] == "floordiv":
+            inner = mono[0]
+            x, b = dict(inner[1]), dict(inner[2])
+            return _poly_floordiv(x, _pmul(b, pb))
+    return _atom(k, pa, pb)
+
+
+def _poly_floordiv(px, pd):
+    """Canonical x // d for polynomials (re-enters the floordiv rules)."""
+    cd = _pconst(pd)
+    if cd is not None and cd != 0 and all(c % cd == 0 for c in px.values()):
+        return {m: c // cd for m, c in px.items()}
+    return _atom("floordiv", px, pd)
+
+
+def canonical(e):
+    """Hashable normal form of ``e`` (see the block comment above)."""
+    return _pkey(_poly(lift(e).node))

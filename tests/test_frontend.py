@@ -125,3 +125,65 @@ def test_builder_defined_specs_typecheck():
     checks = [(S.text(a), S.text(b)) for a, b in fr.grid.checks]
     assert ("cdiv(q_size_2, BLOCK_SIZE_M)", "cdiv(sin_q_size_0, BLOCK_SIZE_M)") in checks
     assert [S.text(s) for s in rp.index_maps["input"].nest_sizes] == ["cdiv(input_size_3, HALF_D)"]
+
+
+@pytest.mark.parametrize("kernel", C.CATALOG_NAMES)
+def test_maps_canonically_equal_to_reference(kernel):
+    """The backend fingerprints maps by canonical form (symbolic.canonical),
+    so a spec built in any association/commutation order matches; the
+    reference's own trees must have the same canonical forms as ours."""
+    ref = maps()[kernel]
+    ck = C.checked(kernel)
+    canon = S.canonical
+    assert [canon(s) for s in ck.grid.sizes] == [canon(S.from_tree(t)) for t in ref["grid"]["sizes"]]
+    for name, m in ck.index_maps.items():
+        r = ref["maps"][name]
+        assert canon(m.offset) == canon(S.from_tree(r["offset"]))
+        assert [canon(a) for a, _ in m.mask] == [canon(S.from_tree(a)) for a, _ in r["mask"]]
+
+
+def test_canonical_form_identities():
+    a, b, c = S.var("a"), S.var("b"), S.var("c")
+    assert S.canonical(a * (b * c)) == S.canonical((c * a) * b)
+    assert S.canonical((a * b + a * c) // a) == S.canonical(b + c)
+    assert S.canonical((a * 6 + 3 * b) % 3) == S.canonical(S.lit(0))
+    assert S.canonical((a // b) // c) == S.canonical(a // (c * b))
+    assert S.canonical(S.emin(a, b)) == S.canonical(S.emin(b, a))
+    assert S.canonical(a // b) != S.canonical(a % b)
+    assert S.canonical(a - a + b * 0) == S.canonical(S.lit(0))
+
+
+def test_decompose_pid_matches_reference_points():
+    from paper_2507_11978_b200.arrange import decompose_pid
+    from helpers import map_cases
+
+    index, arrays = map_cases()
+    for ci, case in enumerate(index):
+        ck = C.checked(case["kernel"])
+        pids = arrays[f"c{ci}_pids"]
+        for p in range(pids.shape[0]):
+            assert decompose_pid(ck.grid, p, case["binding"]) == tuple(int(v) for v in pids[p])
+    with pytest.raises(ArrangeError):
+        decompose_pid(ck.grid, pids.shape[0], case["binding"])
+
+
+def test_flatten_of_flattened_dims_decodes_one_level_deep():
+    """flatten(flatten(x)) == flatten over all dims at once (same maps)."""
+    t = param_with_shape("x", (3, 4, 5))
+    once = t.flatten(0, 3).tile((7,))
+    twice = t.flatten(0, 2).flatten(0, 2).tile((7,))
+    a, b = lower([("x", once)]), lower([("x", twice)])
+    assert a[0].offset == b[0].offset and a[0].mask == b[0].mask
+
+
+def test_inner_views_compose_with_outer_rewrites():
+    """with_inner keeps the substitutions of both views (mm's
+    `input_tiled.dtype = input_tiled.dtype.squeeze(0)` pattern)."""
+    x = param_with_shape("x", (8, 6)).tile((4, 3)).tile((1, -1))
+    y = x.with_inner(x.inner().squeeze(0))
+    m = lower([("x", y)])[0]
+    assert len(m.nest_sizes) == 1 and len(m.lane_sizes) == 2
+    env = {"x_stride_0": 6, "x_stride_1": 1, "pid_0": 1, "pid_1": 0, "nest_0": 1,
+           "lane_0": 2, "lane_1": 1}
+    # row 4*1 + 2, column 3*1 + 1
+    assert S.evaluate(m.offset, env) == 6 * 6 + 4
