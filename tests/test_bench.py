@@ -1,5 +1,5 @@
-"""bench.py contract on CPU: the reference arm (the oracle port timed on the
-host) prints the driver's JSON line, and the roofline / L2-rotation helpers
+"""bench.py contract on CPU: the reference arm (tiledsl sim.launch from
+baseline/_ref, or the oracle port when it is absent) prints the driver's JSON line, and the roofline / L2-rotation helpers
 compute what DESIGN.md section 6 says.  The device arm needs a B200."""
 
 import json
@@ -26,17 +26,18 @@ def test_reference_arm_json_line():
         assert k in line, k
     assert line["impl"] == "reference" and line["metric"] == bench.METRIC
     assert line["steps"] == 1 and line["warmup"] == 3 and line["value"] > 0
-    assert line["cpu_baseline"]["kind"] in ("port", "reference")
+    assert line["cpu_baseline"]["kind"] == ("reference" if bench.reference_available() else "port")
+    assert line["config"]["same_config"] and line["config"]["rows"] == bench.R
     assert line["cpu_baseline"]["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
 
 
 def test_roofline_fraction():
-    w = bench.Work("x", "hbm", 1e9, None, None)
+    w = bench.Work("x", "hbm", 1, lambda n: 1e9 * n, None, None)
     r = bench._roofline(w, 1.0, {"hbm": 2000.0, "tc": 1000.0}, 123)
     assert r["achieved"] == pytest.approx(1000.0) and r["frac"] == pytest.approx(0.5)
     assert r["unit"] == "GB/s" and r["traffic"] == 123
-    w = bench.Work("y", "tensor", 2e12, None, None)
+    w = bench.Work("y", "tensor", 2, lambda n: 1e12 * n, None, None)
     r = bench._roofline(w, 2.0, {"hbm": 2000.0, "tc": 1000.0}, None)
     assert r["achieved"] == pytest.approx(1000.0) and r["frac"] == pytest.approx(1.0)
     assert r["unit"] == "TFLOP/s"
@@ -54,3 +55,10 @@ def test_peaks_and_traffic_files():
     assert pk["hbm"] > 0 and pk["tc"] > 0
     tr = bench.ncu_traffic()
     assert all(v > 0 for k, v in tr.items() if not k.startswith("_"))
+
+
+def test_compare_policy():
+    ok = bench.compare([1.0, 2.0], [1.0, 2.01], 1e-2, 0.0)
+    assert ok["ok"] and ok["max_err"] == pytest.approx(0.01)
+    bad = bench.compare([1.0, float("nan")], [1.0, 1.0], 1e-2, 1e-2)
+    assert not bad["ok"]

@@ -1,8 +1,15 @@
 """Multi-process (gloo, world_size 2, CPU) coverage of the sharding /
-max-over-ranks / verification-gather logic used by bench.py --gpus N."""
+max-over-ranks / verification-gather logic used by bench.py --gpus N - both
+through paper_2507_11978_b200.dist directly and through bench.py's own
+self-spawn + shard + verify path (``--cpu-check``: the oracle stands in for
+the kernels, gloo for NCCL)."""
 
+import json
 import os
 import socket
+import subprocess
+import sys
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -66,3 +73,26 @@ def test_two_rank_gloo_shard_and_verify():
     assert res[0][2] == res[1][2] and len(res[0][2]) == 2
     assert max(res[0][2]) == 0.0
     assert res[0][3] == (0, 32) and res[1][3] == (32, 64)
+
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_gpus_n_self_spawns_and_shards(world):
+    """`bench.py --gpus N` re-executes under torch.distributed.run, each rank
+    builds its row shard of ONE global problem, the timing is the max over
+    ranks, and one gather of per-rank errors verifies every shard."""
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", str(world),
+                          "--cpu-check", "--steps", "3", "--warmup", "3", "--cpu-rows", "100"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    line = json.loads(lines[0])
+    assert line["impl"] == "cpu-check" and line["n_gpus"] == world
+    assert line["shard_starts"] == [float(shard_range(100, r, world)[0]) for r in range(world)]
+    assert line["verify"]["ok"] and len(line["verify"]["max_err_over_tol_per_rank"]) == world
+    assert line["value"] > 0 and line["scaling"] == "strong"

@@ -385,6 +385,114 @@ def test_sdpa_rope_fused(dtype, bshd):
     assert (o.float() - o2.float()).abs().max().item() <= 2e-3
 
 
+def _attn_fp32(q, k, v):
+    """Exact attention in fp32 on the GPU, one batch at a time (no TF32):
+    the all-heads check at the BASELINE shape."""
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        out = torch.empty(q.shape, device=DEV, dtype=torch.float32)
+        for b in range(q.shape[0]):
+            qb, kb, vb = (t[b].float() for t in (q, k, v))
+            s_ = (qb @ kb.transpose(-1, -2)) * (1.0 / np.sqrt(q.shape[-1]))
+            out[b] = torch.softmax(s_, dim=-1) @ vb
+        return out
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def _attn_close_all_heads(o, ref, rtol=1e-2, atol=1e-2):
+    bad = ((o.float() - ref).abs() > atol + rtol * ref.abs()).sum().item()
+    assert bad == 0, f"{bad} outputs outside tol; max err {(o.float() - ref).abs().max().item():.3e}"
+
+
+# deterministic head subset checked against the f64 oracle (first, last and
+# a few in between)
+_BASELINE_HEADS = [(0, 0), (5, 17), (13, 31), (22, 3), (31, 31)]
+
+
+def test_sdpa_baseline_shape():
+    """B32 H32 S4096 D128 (BASELINE configs[4]): 32 KV tiles per query block,
+    many lazy-rescale events.  All heads vs exact fp32 attention on the GPU,
+    a head subset vs the f64 oracle."""
+    g = torch.Generator(device=DEV).manual_seed(4096)
+    shp = (32, 32, 4096, 128)
+    q, k, v = ((torch.rand(shp, generator=g, device=DEV) * 2 - 1).half() for _ in range(3))
+    o = torch.empty(shp, device=DEV, dtype=torch.float16)
+    with _Paths() as pc:
+        backend.sdpa_launch(q, k, v, o, 128, 128)
+        torch.cuda.synchronize()
+    assert pc.delta["attn_tc"] == 1
+    _attn_close_all_heads(o, _attn_fp32(q, k, v))
+    for b, h in _BASELINE_HEADS:
+        ref = oracle.sdpa(q[b, h].float().cpu().numpy(), k[b, h].float().cpu().numpy(),
+                          v[b, h].float().cpu().numpy())
+        _close(o[b, h], ref)
+
+
+def test_sdpa_rope_baseline_shape():
+    """sdpa(rope(q), rope(k), v) at B32 H32 S4096 D128 with (B, S, H, D)
+    storage: all heads vs fp32 attention over the rotated (device-rounded)
+    Q/K, a head subset vs the f64 oracle."""
+    g = torch.Generator(device=DEV).manual_seed(4097)
+    b_, s_, h_, d_ = 32, 4096, 32, 128
+    base = [(torch.rand((b_, s_, h_, d_), generator=g, device=DEV) * 2 - 1).half() for _ in range(3)]
+    ang = torch.rand((s_, d_ // 2), generator=g, device=DEV) * 6 - 3
+    sn, cs = torch.sin(ang).half(), torch.cos(ang).half()
+    q, k, v = (t.transpose(1, 2) for t in base)
+    o = torch.empty((b_, h_, s_, d_), device=DEV, dtype=torch.float16)
+    backend.sdpa_rope_launch(q, k, v, sn, cs, sn, cs, o, 128, 128)
+    torch.cuda.synchronize()
+
+    def rot(x):                                  # (B, H, S, D) fp32 rotation, then fp16
+        x = x.float()
+        c, s = cs.float()[None, None], sn.float()[None, None]
+        x0, x1 = x[..., :d_ // 2], x[..., d_ // 2:]
+        return torch.cat([x0 * c - x1 * s, x0 * s + x1 * c], -1).half()
+
+    qr, kr = rot(q), rot(k)
+    _attn_close_all_heads(o, _attn_fp32(qr, kr, v))
+    del qr, kr
+    snp, csp = sn.float().cpu().numpy(), cs.float().cpu().numpy()
+    for b, h in _BASELINE_HEADS[:3]:
+        qq, kk, vv = (t[b:b + 1, h:h + 1].float().cpu().numpy() for t in (q, k, v))
+        ref = oracle.sdpa_rope(qq, kk, vv, snp, csp, snp, csp, round_to=np.float16)[0, 0]
+        _close(o[b, h], ref)
+
+
+def test_repeat_launch_bit_identity():
+    """The reference pins reversed / repeated launches as bit-identical
+    (test_acceptance.py:165-172).  The persistent / narrow-tail schedules here
+    must be too: launch each twice (and once more after other work) and
+    compare bytes."""
+    g = torch.Generator(device=DEV).manual_seed(3)
+
+    def U(*shape):
+        return (torch.rand(shape, generator=g, device=DEV) * 2 - 1).half()
+
+    cases = []
+    a, b = U(2560, 1024), U(1024, 4096)          # mm with a narrow tail wave
+    cases.append(lambda out: backend.mm_launch(a, b, out, 128, 128, 64))
+    x, w = U(4, 64, 30, 30), U(256, 64, 3, 3)    # conv2d, several tiles + tail
+    cases.append(lambda out: backend.conv2d_launch(x, w, out, 128, 128, 64))
+    q, k, v = U(3, 64, 700, 128), U(3, 64, 700, 128), U(3, 64, 700, 128)   # > 148 items
+    cases.append(lambda out: backend.sdpa_launch(q, k, v, out, 128, 128))
+    shapes = [(2560, 4096), (4, 256, 28, 28), (3, 64, 700, 128)]
+    firsts = []
+    for fn, shp in zip(cases, shapes):
+        o1, o2 = (torch.full(shp, float("nan"), device=DEV, dtype=torch.float16) for _ in range(2))
+        fn(o1)
+        fn(o2)
+        torch.cuda.synchronize()
+        assert torch.equal(o1, o2)
+        firsts.append((fn, o1))
+    for fn, ref in firsts:                       # again, after everything else ran
+        o3 = torch.full(ref.shape, float("nan"), device=DEV, dtype=torch.float16)
+        fn(o3)
+        torch.cuda.synchronize()
+        assert torch.equal(o3, ref)
+
+
 def test_sdpa_strided_views():
     """(B, S, H, D) storage viewed as (B, H, S, D) (rope output layout)."""
     rng = np.random.default_rng(5)
