@@ -272,7 +272,10 @@ def compare(got, ref, rtol: float, atol: float) -> dict:
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     diff = np.abs(got - ref)
-    ratio = float((diff / (atol + rtol * np.abs(ref))).max()) if diff.size else 0.0
+    tol = atol + rtol * np.abs(ref)
+    # tol == 0 (bit-exact checks): 0 where exact, inf where not
+    over = np.divide(diff, tol, out=np.where(diff > 0, np.inf, 0.0), where=tol > 0)
+    ratio = float(over.max()) if diff.size else 0.0
     return {"max_err": float(diff.max()) if diff.size else 0.0, "max_err_over_tol": round(ratio, 4),
             "rtol": rtol, "atol": atol, "ok": bool(ratio <= 1.0 and np.isfinite(got).all())}
 
