@@ -727,11 +727,6 @@ int attn_sm100(const AttnDesc& a, int dtype, cudaStream_t s, const RopeTables* r
     return bf16 ? launch_attn<64, true, true>(maps, p, s) : launch_attn<64, false, true>(maps, p, s);
   }
   if (dry_run) return NTB_OK;
-  static const bool pair = getenv("NTB_ATTN_PAIR") && atoi(getenv("NTB_ATTN_PAIR")) == 1;
-  if (pair && a.D == 128) {
-    const int rc = attn_pair_sm100(a, dtype, s);
-    if (rc != NTB_ERR_UNSUPPORTED) return rc;
-  }
   if (a.D == 128)
     return bf16 ? launch_attn<128, true, false>(maps, p, s) : launch_attn<128, false, false>(maps, p, s);
   return bf16 ? launch_attn<64, true, false>(maps, p, s) : launch_attn<64, false, false>(maps, p, s);

@@ -23,7 +23,5 @@ int rope_rows_vec(const void* x, const void* sn, const void* cs, void* out, int6
 // dry_run: validate the layout contract (and build the tensor maps) without launching.
 int attn_sm100(const AttnDesc& a, int dtype, cudaStream_t s, const RopeTables* rope = nullptr,
                bool dry_run = false);
-// CTA-pair variant (k_attn_pair_sm100.cu), D = 128, no rope.
-int attn_pair_sm100(const AttnDesc& a, int dtype, cudaStream_t s);
 
 }  // namespace ntb

@@ -822,20 +822,3 @@ def test_workspace_is_per_stream():
             assert torch.equal(args[-1], ref)
     ref = torch.nn.functional.conv2d(xb.float(), wb.float())
     assert (yb.float() - ref).abs().max().item() < 0.5
-
-
-@pytest.mark.parametrize("shape", [("1", "2", "256", "128"), ("2", "3", "1000", "128")])
-def test_sdpa_pair_kernel_opt_in(shape):
-    """The experimental CTA-pair attention kernel (NTB_ATTN_PAIR=1, read once
-    per process, so it runs in a subprocess) against torch's fp32 SDPA."""
-    import os
-    import re
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, NTB_ATTN_PAIR="1")
-    out = subprocess.run([sys.executable, os.path.join(root, "tools", "one_case.py"), "sdpa",
-                          *shape], capture_output=True, text=True, timeout=300, cwd=root, env=env)
-    assert out.returncode == 0, out.stderr[-2000:]
-    err = float(re.search(r"sdpa max err ([0-9.e+-]+)", out.stdout).group(1))
-    assert err < 2e-3 and "'attn_tc': 1" in out.stdout
