@@ -731,7 +731,9 @@ def headline(args, ctx, pk):
 
     step_bytes = (2 * rows * C * 2) + (2 * rows * C * 2 + C * 2)      # this rank
     job_bytes = (2 * R * C * 2) + (2 * R * C * 2 + C * 2)              # the whole problem
-    nsets = _sets_for(step_bytes)
+    # sized on ONE kernel's bytes: the per-kernel graphs (g_sm, g_rms) touch
+    # one input/output pair per call, and must also rotate > 3x the L2
+    nsets = _sets_for(2 * rows * C * 2)
     w = rows_input(ctx, 0, 1, C, seed=7)[0]
     # set 0 = rows [lo, hi) of the global seeded problem (what verify checks);
     # the other rotating sets are fresh device-random rows
