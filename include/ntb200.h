@@ -83,7 +83,8 @@ enum {
   NTB_PATH_REPACK = 13,
   NTB_PATH_ROW_STREAM = 14,
   NTB_PATH_JIT = 15,
-  NTB_NUM_PATHS = 16
+  NTB_PATH_GEMM_TF32 = 16,  /* fp32 mm/bmm/addmm: 3xTF32 on tcgen05 */
+  NTB_NUM_PATHS = 17
 };
 int64_t ntb_path_count(int path);
 

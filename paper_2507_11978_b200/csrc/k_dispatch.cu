@@ -2,6 +2,8 @@
 // (mm / bmm / addmm, conv2d, sdpa).  Fast sm_100a tcgen05 kernels take the
 // layouts they support; everything else runs the generic CUDA-core kernels
 // (k_generic.cu).  Nothing here ever computes on the host.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "k_generic.cuh"
 #include "k_sm100.cuh"
@@ -58,6 +60,14 @@ int launch_gemm(const LaunchArgs& A) {
   if (A.dtype == NTB_F16 || A.dtype == NTB_BF16) {
     int rc = gemm_sm100(g, A.dtype, A.stream);
     if (rc != NTB_ERR_UNSUPPORTED) return rc;
+  } else if (A.dtype == NTB_F32) {
+    // the reference catalog's own dtype (catalog.py:125-129): 3xTF32 on the
+    // tensor cores; NTB_GEMM_F32_FMA=1 forces the CUDA-core kernel (A/B only)
+    static const bool fma_only = getenv("NTB_GEMM_F32_FMA") != nullptr;
+    if (!fma_only) {
+      int rc = gemm_tf32_sm100(g, A.stream);
+      if (rc != NTB_ERR_UNSUPPORTED) return rc;
+    }
   }
   return gemm_generic(g, A.dtype, A.stream);
 }
