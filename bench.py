@@ -62,6 +62,13 @@ REF_DIR = ROOT / "baseline" / "_ref"
 # fp16 row kernels: fp32 arithmetic, <= 1 ulp of the fp16 output (DESIGN 4)
 ROW_TOL = (2.0 ** -9, 1e-7)
 HALF_TOL = (1e-2, 1e-2)       # SURVEY 8(c) policy for fp16 contractions / attention
+TF32X3_PEAK_SCALE = 1.0 / 6.0   # tf32 dense rate = bf16 / 2; 3 MMAs per fp32 product
+
+
+def F32_MM_TOL(k):
+    """fp32 contractions (tests/test_gpu_tf32.py): the reference's 1e-4
+    (verify.py:24-25) grown with sqrt(K / 64), plus 1e-5 relative."""
+    return (1e-5, 1e-4 * max(1.0, (k / 64.0) ** 0.5))
 
 
 def peaks():
@@ -330,8 +337,10 @@ class Work:
     verification against the oracle."""
 
     def __init__(self, name, bound, total, cost, setup, call, check=None, note="", torch_op=None,
-                 split=""):
+                 split="", peak_scale=1.0):
         self.name, self.bound, self.total, self.cost = name, bound, total, cost
+        # tensor peak of this kernel's instruction kind relative to dense bf16
+        self.peak_scale = peak_scale
         self.setup, self.call, self.check, self.note = setup, call, check, note
         self.split = split
         # (description, fn(set)): the same op through PyTorch's own library
@@ -475,6 +484,57 @@ def build_works(ctx, which):
                         torch_op=("torch.bmm(a, b, out=c) (cuBLAS)",
                                   lambda a: torch.bmm(a["a"], a["b"], out=a["c"])),
                         split="batch")
+
+    # -- fp32 mm / bmm (the reference catalog's own dtype, catalog.py:125-129):
+    # 3xTF32 on the tensor cores; peak = dense tf32 (half the bf16 rate) / 3
+    # MMAs per useful product.  Library point: cuBLAS SGEMM (allow_tf32 off).
+    f32 = torch.float32
+
+    def mm32_setup(lo, hi):
+        n = hi - lo
+        k = _sets_for((2 * n * MM + MM * MM) * 4)
+        return [dict(a=U((n, MM), f32), b=U((MM, MM), f32), c=E((n, MM), f32)) for _ in range(k)]
+
+    def mm32_check(a):
+        n = a["a"].shape[0]
+        idx = torch.arange(0, n, max(1, n // 8), device=dev)
+        ref = oracle.mm(_np(a["a"][idx]), _np(a["b"]))
+        return compare(_np(a["c"][idx]), ref, *F32_MM_TOL(MM))
+
+    def sgemm(fn):
+        def run(a):
+            prev = torch.backends.cuda.matmul.allow_tf32
+            torch.backends.cuda.matmul.allow_tf32 = False
+            try:
+                return fn(a)
+            finally:
+                torch.backends.cuda.matmul.allow_tf32 = prev
+        return run
+
+    works["mm_f32"] = Work("mm fp32 4096^3 (3xTF32 tcgen05)", "tensor", MM, mm_cost, mm32_setup,
+                           lambda a: B.mm_launch(a["a"], a["b"], a["c"], 128, 128, 64), mm32_check,
+                           torch_op=("torch.mm(a, b, out=c) fp32, allow_tf32=False (cuBLAS SGEMM)",
+                                     sgemm(lambda a: torch.mm(a["a"], a["b"], out=a["c"]))),
+                           split="rows of A / C", peak_scale=TF32X3_PEAK_SCALE)
+
+    def bmm32_setup(lo, hi):
+        n = hi - lo
+        k = _sets_for(3 * n * 1024 * 1024 * 4)
+        return [dict(a=U((n, 1024, 1024), f32), b=U((n, 1024, 1024), f32),
+                     c=E((n, 1024, 1024), f32)) for _ in range(k)]
+
+    def bmm32_check(a):
+        b = a["a"].shape[0] - 1
+        rows = torch.arange(0, 1024, 128, device=dev)
+        ref = oracle.mm(_np(a["a"][b][rows]), _np(a["b"][b]))
+        return compare(_np(a["c"][b][rows]), ref, *F32_MM_TOL(1024))
+
+    works["bmm_f32"] = Work("bmm fp32 64x1024^3 (3xTF32 tcgen05)", "tensor", 64,
+                            lambda n: 2 * n * 1024 ** 3, bmm32_setup,
+                            lambda a: B.bmm_launch(a["a"], a["b"], a["c"], 128, 128, 64), bmm32_check,
+                            torch_op=("torch.bmm(a, b, out=c) fp32, allow_tf32=False (cuBLAS SGEMM)",
+                                      sgemm(lambda a: torch.bmm(a["a"], a["b"], out=a["c"]))),
+                            split="batch", peak_scale=TF32X3_PEAK_SCALE)
 
     # -- conv2d: images sharded
     def conv_setup(lo, hi):
@@ -658,9 +718,13 @@ def _roofline(work, ms, pk, traffic):
         peak, unit = pk["hbm"], "GB/s"
     else:
         achieved = work.units / (ms * 1e-3) / 1e12
-        peak, unit = pk["tc"], "TFLOP/s"
-    return {"bound": work.bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
-            "frac": round(achieved / peak, 4), "traffic": traffic}
+        peak, unit = round(pk["tc"] * work.peak_scale, 2), "TFLOP/s"
+    r = {"bound": work.bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
+         "frac": round(achieved / peak, 4), "traffic": traffic}
+    if work.peak_scale != 1.0:
+        r["peak_note"] = ("dense tf32 = 1/2 of the measured bf16 peak, / 3 tf32 MMAs per useful "
+                          "fp32 product (3xTF32)")
+    return r
 
 
 def run_kernels(ctx, args, pk, sel):
@@ -678,7 +742,7 @@ def run_kernels(ctx, args, pk, sel):
             ms, launches, clk = time_work(ctx, wk, sets, steps, 2)
             # whole-job rate: the full problem's units over the slowest rank
             roof = _roofline(wk, ms, pk, traffic.get(key) if ctx.world == 1 else None)
-            if wk.bound == "tensor" and pk.get("tc_sus"):
+            if wk.bound == "tensor" and pk.get("tc_sus") and wk.peak_scale == 1.0:
                 # the same achieved rate against the sustained (power-capped)
                 # tensor peak, for reading alongside sm_mhz
                 roof["frac_of_sustained"] = round(roof["achieved"] / pk["tc_sus"], 4)
@@ -1165,6 +1229,7 @@ def B_paths():
 
 
 KERNELS = ["add_2^20", "add_2^24", "silu_2^24", "softmax", "rms_norm", "mm", "addmm", "bmm",
+           "mm_f32", "bmm_f32",
            "conv2d", "sdpa", "sdpa_paper", "rope", "sdpa_rope", "rope+sdpa"]
 
 
