@@ -536,6 +536,36 @@ def build_works(ctx, which):
                                       sgemm(lambda a: torch.bmm(a["a"], a["b"], out=a["c"]))),
                             split="batch", peak_scale=TF32X3_PEAK_SCALE)
 
+    def conv32_setup(lo, hi):
+        n = hi - lo
+        k = _sets_for((n * 256 * 56 * 56 + n * 256 * 54 * 54) * 4)
+        w = U((256, 256, 3, 3), f32)
+        return [dict(x=U((n, 256, 56, 56), f32), w=w, y=E((n, 256, 54, 54), f32)) for _ in range(k)]
+
+    def conv32_check(a):
+        i = a["x"].shape[0] - 1
+        ref = oracle.conv2d(_np(a["x"][i:i + 1]), _np(a["w"]))
+        return compare(_np(a["y"][i:i + 1]), ref, *F32_MM_TOL(256 * 9))
+
+    def no_tf32_conv(fn):
+        def run(a):
+            prev = torch.backends.cudnn.allow_tf32
+            torch.backends.cudnn.allow_tf32 = False
+            try:
+                return fn(a)
+            finally:
+                torch.backends.cudnn.allow_tf32 = prev
+        return run
+
+    works["conv2d_f32"] = Work(
+        "conv2d fp32 N64 C256 56x56 K256 3x3 (3xTF32 tcgen05)", "tensor", 64,
+        lambda n: 2 * n * 54 * 54 * 256 * 256 * 9, conv32_setup,
+        lambda a: B.conv2d_launch(a["x"], a["w"], a["y"], 128, 128, 64), conv32_check,
+        torch_op=("torch.nn.functional.conv2d(x, w) fp32, cudnn.allow_tf32=False (cuDNN)",
+                  no_tf32_conv(lambda a: torch.nn.functional.conv2d(a["x"], a["w"]))),
+        note="includes the per-call filter repack and NCHW -> pixel-major copy",
+        split="images", peak_scale=TF32X3_PEAK_SCALE)
+
     # -- conv2d: images sharded
     def conv_setup(lo, hi):
         n = hi - lo
@@ -1229,7 +1259,7 @@ def B_paths():
 
 
 KERNELS = ["add_2^20", "add_2^24", "silu_2^24", "softmax", "rms_norm", "mm", "addmm", "bmm",
-           "mm_f32", "bmm_f32",
+           "mm_f32", "bmm_f32", "conv2d_f32",
            "conv2d", "sdpa", "sdpa_paper", "rope", "sdpa_rope", "rope+sdpa"]
 
 

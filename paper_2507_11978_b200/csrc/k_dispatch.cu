@@ -104,6 +104,12 @@ int launch_conv2d(const LaunchArgs& A) {
   if (A.dtype == NTB_F16 || A.dtype == NTB_BF16) {
     int rc = conv_sm100(c, A.dtype, A.stream);
     if (rc != NTB_ERR_UNSUPPORTED) return rc;
+  } else if (A.dtype == NTB_F32) {
+    static const bool fma_only = getenv("NTB_GEMM_F32_FMA") != nullptr;
+    if (!fma_only) {
+      int rc = conv_tf32_sm100(c, A.stream);
+      if (rc != NTB_ERR_UNSUPPORTED) return rc;
+    }
   }
   return conv_generic(c, A.dtype, A.stream);
 }

@@ -64,6 +64,12 @@ struct TParams {
   float alpha, beta;
   int has_d;
   int passes;   // 3 (default); 1 = plain TF32 (NTB_TF32_PASSES=1, A/B only)
+  // conv2d (implicit GEMM, CONV = true): A = filter W'[k][(r,s)][c4],
+  // B = image X'[n][pixel][c4]; `batch` = N images, tiles of 256 output
+  // channels x 256 virtual pixels (row width W, the W - Q tail discarded)
+  int cb, pix_tiles, k_tiles, S, W, PW, Q, RS;
+  float* y;
+  int64_t ys[4];
 };
 
 __host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn, int M, int N) {
@@ -125,7 +131,7 @@ __device__ __forceinline__ uint64_t tdesc(uint32_t addr, int k) {
             : sm100::umma_desc_sw128(addr + k * 32, 16, 1024);
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, bool CONV>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
     gemm_tf32_kernel(const __grid_constant__ TMaps maps, const TParams p) {
   using namespace sm100;
@@ -139,9 +145,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
-  const int tiles_per_batch = p.num_m * p.num_n;
+  // GEMM tile t = (batch, n tile, m tile); conv tile t = (image, pixel tile, channel tile)
+  const int tiles_per_batch = CONV ? p.pix_tiles * p.k_tiles : p.num_m * p.num_n;
   const int total = tiles_per_batch * p.batch;
-  const int nk = (p.K + TBK - 1) / TBK;
+  const int nk = CONV ? p.RS * p.cb : (p.K + TBK - 1) / TBK;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
   if (threadIdx.x == 0) {
@@ -159,7 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&maps.a);
     tma_prefetch(&maps.b);
-    tma_prefetch(&maps.c);
+    if (!CONV) tma_prefetch(&maps.c);
   }
   if (warp == 2) {
     tmem_alloc_pair(&tmem_slot, T_TMEM_COLS);
@@ -177,13 +184,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
       uint32_t ph = 0;
       for (int t = cid; t < total; t += ncl) {
         const int b = t / tiles_per_batch, r = t % tiles_per_batch;
-        const int nt = r / p.num_m, mt = r % p.num_m;
+        // conv: pixel tile = r / k_tiles ("n" role), channel tile = r % k_tiles ("m" role)
+        const int nt = CONV ? r / p.k_tiles : r / p.num_m, mt = CONV ? r % p.k_tiles : r % p.num_m;
         const int row = mt * 256 + (int)rank * 128, col = nt * 256 + (int)rank * 128;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[st], ph ^ 1);
           mbar_expect_tx(&full[st], 2 * T_TILE);
           uint8_t* a_dst = smem + st * T_STAGE;
           uint8_t* b_dst = a_dst + T_TILE;
+          if constexpr (CONV) {
+            // K order (r, s) outer, 32-channel blocks inner; the image rows of
+            // tap (r, s) are the tile's virtual pixels shifted by r * W + s
+            const int rs = kb / p.cb, cbk = kb % p.cb;
+            const int shift = (rs / p.S) * p.W + (rs % p.S);
+            tma_load_3d(a_dst, &maps.a, &full[st], cbk * TBK, rs, row);
+            tma_load_3d(b_dst, &maps.b, &full[st], cbk * TBK, col + shift, b);
+          } else {
           if (!A_MN) {
             tma_load_3d(a_dst, &maps.a, &full[st], kb * TBK, row, b);
           } else {
@@ -197,6 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
 #pragma unroll
             for (int c = 0; c < 4; ++c)
               tma_load_3d(b_dst + c * (TBK * 128), &maps.b, &full[st], col + c * 32, kb * TBK, b);
+          }
           }
           if (++st == T_STAGES) {
             st = 0;
@@ -312,7 +329,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
     int g = 0;
     for (int t = cid; t < total; t += ncl) {
       const int b = t / tiles_per_batch, r = t % tiles_per_batch;
-      const int nt = r / p.num_m, mt = r % p.num_m;
+      const int nt = CONV ? r / p.k_tiles : r / p.num_m, mt = CONV ? r % p.k_tiles : r % p.num_m;
       float acc[128];
       for (int c = 0; c < nchunks; ++c, ++g) {
         mbar_wait(&tfull[g & 1], (g >> 1) & 1);
@@ -330,6 +347,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(leader_addr(&tempty[g & 1]));
+      }
+      if constexpr (CONV) {
+        // this thread: output channel k0 + lane, virtual pixels pix0 + [0, 128).
+        // Each 32 x 32 block goes through shared memory (element (row, col)
+        // at col * 32 + (row + col) % 32: conflict-free both ways) so that a
+        // warp's stores run along the output row of one channel
+        const int k0 = mt * 256 + (int)rank * 128 + quad * 32;
+        const int pix0 = nt * 256 + half * 128;
+        float* xp = reinterpret_cast<float*>(stage);
+        const int kn = p.K - k0;
+        float* ybase = p.y + (int64_t)b * p.ys[0] + (int64_t)k0 * p.ys[1];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) xp[i * 32 + ((lane + i) & 31)] = acc[q * 32 + i];
+          __syncwarp();
+          const int m = pix0 + q * 32 + lane;
+          const int pp = m / p.W, qq = m - pp * p.W;
+          const bool ok = m < p.PW && qq < p.Q;
+          float* yp = ybase + (int64_t)pp * p.ys[2] + (int64_t)qq * p.ys[3];
+          if (kn >= 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float f = xp[lane * 32 + ((j + lane) & 31)];
+              if (ok) yp[(int64_t)j * p.ys[1]] = f;
+            }
+          } else {
+            for (int j = 0; j < kn; ++j) {
+              const float f = xp[lane * 32 + ((j + lane) & 31)];
+              if (ok) yp[(int64_t)j * p.ys[1]] = f;
+            }
+          }
+        }
+        continue;
       }
       const int row0 = mt * 256 + (int)rank * 128 + quad * 32;
       const int row = row0 + lane;
@@ -386,18 +438,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
   }
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, bool CONV = false>
 int launch_tf32(const TMaps& maps, const TParams& p, cudaStream_t s) {
-  auto k = gemm_tf32_kernel<A_MN, B_MN>;
+  auto k = gemm_tf32_kernel<A_MN, B_MN, CONV>;
   static size_t attr[kMaxDevices] = {};
   cudaError_t e = smem_attr_once(k, T_SMEM, attr);
   if (e != cudaSuccess) return cuda_fail(e, "gemm tf32 smem attribute");
-  const int total = p.num_m * p.num_n * p.batch;
+  const int total = (CONV ? p.pix_tiles * p.k_tiles : p.num_m * p.num_n) * p.batch;
   int clusters = sm_count() / 2;
   if (total < clusters) clusters = total;
   e = launch_pdl(k, dim3(2 * clusters), dim3(T_THREADS), T_SMEM, s, maps, p);
   if (e != cudaSuccess) return cuda_fail(e, "gemm tf32 launch");
-  return check_launch("gemm 3xtf32 tcgen05 pair", NTB_PATH_GEMM_TF32);
+  return check_launch(CONV ? "conv2d 3xtf32 tcgen05 pair" : "gemm 3xtf32 tcgen05 pair",
+                      CONV ? NTB_PATH_CONV_TF32 : NTB_PATH_GEMM_TF32);
 }
 
 bool ok_stride4(int64_t elems) { return elems > 0 && (elems * 4) % 16 == 0; }
@@ -473,6 +526,124 @@ int gemm_tf32_sm100(const GemmDesc& g, cudaStream_t s) {
   p.passes = passes;
   if (a_mn) return b_mn ? launch_tf32<true, true>(maps, p, s) : launch_tf32<true, false>(maps, p, s);
   return b_mn ? launch_tf32<false, true>(maps, p, s) : launch_tf32<false, false>(maps, p, s);
+}
+
+// ---- conv2d fp32: filter repack + NCHW -> pixel-major transpose, then the
+// same 3xTF32 pair kernel in implicit-GEMM mode ------------------------------
+
+namespace {
+
+// W'[k][rs][c4] <- W[k][c][r][s] (0 for c >= C)
+__global__ void repack_filter_f32(const float* __restrict__ w, int64_t s0, int64_t s1, int64_t s2,
+                                  int64_t s3, float* __restrict__ out, int K, int C, int C4, int R,
+                                  int S) {
+  const int64_t total = (int64_t)K * R * S * C4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C4);
+    const int64_t rest = i / C4;
+    const int rs = (int)(rest % (R * S));
+    const int k = (int)(rest / (R * S));
+    const int r = rs / S, s = rs % S;
+    out[i] = c < C ? w[k * s0 + c * s1 + r * s2 + s * s3] : 0.f;
+  }
+}
+
+// X'[n][pix][c4] <- X[n][c][pix]: 32 channels x 32 pixels per 32 x 8 block
+// through a padded shared tile (coalesced along pixels in, channels out).
+__global__ void __launch_bounds__(256) nchw_to_pixel_major_f32(const float* __restrict__ x,
+                                                               int64_t sn, int64_t sc,
+                                                               float* __restrict__ out, int C,
+                                                               int C4, int HW) {
+  __shared__ float tile[32][33];
+  const int n = blockIdx.z, c0 = blockIdx.y * 32, p0 = blockIdx.x * 32;
+  const float* src = x + (int64_t)n * sn;
+  for (int cy = threadIdx.y; cy < 32; cy += 8) {
+    const int c = c0 + cy, pix = p0 + threadIdx.x;
+    tile[cy][threadIdx.x] = (c < C && pix < HW) ? src[(int64_t)c * sc + pix] : 0.f;
+  }
+  __syncthreads();
+  float* dst = out + (int64_t)n * HW * C4;
+  for (int py = threadIdx.y; py < 32; py += 8) {
+    const int pix = p0 + py, c = c0 + threadIdx.x;
+    if (pix < HW && c < C4) dst[(int64_t)pix * C4 + c] = tile[threadIdx.x][py];
+  }
+}
+
+}  // namespace
+
+int conv_tf32_sm100(const ConvDesc& c, cudaStream_t s) {
+  if (c.N >= 65536 || c.K >= (1 << 30) || (int64_t)c.H * c.W >= (1ll << 31) || c.C >= (1 << 30))
+    return NTB_ERR_UNSUPPORTED;
+  const int64_t HW = c.H * c.W, RS = c.R * c.S;
+  // channels_last fp32 input ([N][H][W][C], C % 4 == 0) is read in place
+  const bool nhwc = c.xs[1] == 1 && c.xs[3] == c.C && c.xs[2] == c.W * c.C &&
+                    (c.N == 1 || c.xs[0] == HW * c.C) && c.C % 4 == 0 && aligned16(c.x);
+  const bool nchw = c.xs[3] == 1 && c.xs[2] == c.W;
+  if (!nhwc && !nchw) return NTB_ERR_UNSUPPORTED;
+  const int64_t C4 = nhwc ? c.C : (c.C + 3) / 4 * 4;
+  const size_t wbytes = ((size_t)c.K * RS * C4 * 4 + 255) / 256 * 256;
+  const size_t xbytes = nhwc ? 0 : (size_t)c.N * HW * C4 * 4;
+  char* ws = (char*)workspace(wbytes + xbytes, s);
+  if (!ws) return fail(NTB_ERR_CUDA, "conv2d: workspace allocation failed");
+  float* wp = reinterpret_cast<float*>(ws);
+  const float* xp = nhwc ? static_cast<const float*>(c.x) : reinterpret_cast<const float*>(ws + wbytes);
+  const int sms = sm_count();
+  {
+    const int64_t total = c.K * RS * C4;
+    int blocks = (int)cdiv64(total, 256);
+    if (blocks > sms * 8) blocks = sms * 8;
+    repack_filter_f32<<<blocks, 256, 0, s>>>(static_cast<const float*>(c.w), c.ws[0], c.ws[1],
+                                             c.ws[2], c.ws[3], wp, (int)c.K, (int)c.C, (int)C4,
+                                             (int)c.R, (int)c.S);
+    int rc = check_launch("conv2d fp32 filter repack", NTB_PATH_REPACK);
+    if (rc) return rc;
+  }
+  if (!nhwc) {
+    dim3 grid((unsigned)cdiv64(HW, 32), (unsigned)cdiv64(C4, 32), (unsigned)c.N);
+    nchw_to_pixel_major_f32<<<grid, dim3(32, 8), 0, s>>>(static_cast<const float*>(c.x), c.xs[0],
+                                                        c.xs[1], const_cast<float*>(xp), (int)c.C,
+                                                        (int)C4, (int)HW);
+    int rc = check_launch("conv2d fp32 NCHW -> pixel-major", NTB_PATH_REPACK);
+    if (rc) return rc;
+  }
+  TMaps maps;
+  const CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  {
+    uint64_t dims[3] = {(uint64_t)C4, (uint64_t)RS, (uint64_t)c.K};
+    uint64_t str[2] = {(uint64_t)C4 * 4, (uint64_t)(RS * C4 * 4)};
+    uint32_t box[3] = {TBK, 1, 128};
+    if (!encode_tmap(&maps.a, dt, 3, wp, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return fail(NTB_ERR_UNSUPPORTED, "conv2d fp32: filter tensor map");
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)C4, (uint64_t)HW, (uint64_t)c.N};
+    uint64_t str[2] = {(uint64_t)C4 * 4, (uint64_t)(HW * C4 * 4)};
+    uint32_t box[3] = {TBK, 128, 1};
+    if (!encode_tmap(&maps.b, dt, 3, xp, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return fail(NTB_ERR_UNSUPPORTED, "conv2d fp32: image tensor map");
+  }
+  maps.c = maps.a;   // unused in conv mode
+  TParams p = {};
+  p.batch = (int)c.N;
+  p.K = (int)c.K;
+  p.cb = (int)cdiv64(c.C, TBK);
+  p.RS = (int)RS;
+  p.S = (int)c.S;
+  p.W = (int)c.W;
+  p.PW = (int)(c.P * c.W);
+  p.Q = (int)c.Q;
+  p.pix_tiles = (int)cdiv64((int64_t)c.P * c.W, 256);
+  p.k_tiles = (int)cdiv64(c.K, 256);
+  p.alpha = 1.f;
+  p.y = static_cast<float*>(c.y);
+  for (int d = 0; d < 4; ++d) p.ys[d] = c.ys[d];
+  static const int passes = [] {
+    const char* e = getenv("NTB_TF32_PASSES");
+    return e && e[0] == '1' ? 1 : 3;
+  }();
+  p.passes = passes;
+  return launch_tf32<false, false, true>(maps, p, s);
 }
 
 }  // namespace ntb

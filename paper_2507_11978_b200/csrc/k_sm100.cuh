@@ -10,6 +10,8 @@ namespace ntb {
 int gemm_sm100(const GemmDesc& g, int dtype, cudaStream_t s);
 // fp32 operands: 3xTF32 (hi*hi + hi*lo + lo*hi) on kind::tf32, CTA pairs.
 int gemm_tf32_sm100(const GemmDesc& g, cudaStream_t s);
+// fp32 conv2d: the same kernel as an implicit GEMM over a pixel-major copy.
+int conv_tf32_sm100(const ConvDesc& c, cudaStream_t s);
 int conv_sm100(const ConvDesc& c, int dtype, cudaStream_t s);
 // Query-side rotary tables for sdpa_rope: {rows, cols, row_stride,
 // col_stride} in elements.  The kernel rotates Q tiles in shared memory; K

@@ -1,6 +1,6 @@
-"""GPU parity of the fp32 contractions (mm / addmm / bmm) on the tensor cores
-(3xTF32, csrc/k_gemm_tf32_sm100.cu) against the CPU oracle (f64 dot rounded
-to f32, the reference's own Dot semantics, sim.py:317-320).
+"""GPU parity of the fp32 contractions (mm / addmm / bmm / conv2d) on the
+tensor cores (3xTF32, csrc/k_gemm_tf32_sm100.cu) against the CPU oracle (f64
+dot rounded to f32, the reference's own Dot semantics, sim.py:317-320).
 
 Tolerance (written here): |got - ref| <= 1e-4 * sqrt(K / 64) + 1e-5 * |ref|
 - the reference's fp32 contraction tolerance (1e-4 max-abs, verify.py:24-25)
@@ -140,3 +140,27 @@ def test_f32_magnitudes():
         ref = oracle.mm(a, b).astype(np.float64)
         err = np.abs(got.cpu().numpy() - ref).max()
         assert err <= 2e-6 * np.abs(ref).max(), (scale, err, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 5, 5, 3, 3, 3), (2, 16, 12, 10, 32, 3, 3),
+                                   (2, 64, 30, 30, 128, 3, 3), (3, 100, 17, 23, 320, 5, 5),
+                                   (9, 64, 40, 40, 64, 1, 1), (4, 256, 56, 56, 256, 3, 3)])
+def test_conv2d_f32_tensor_cores(shape):
+    n, c, h, w, k, r, s = shape
+    rng = np.random.default_rng(n * 31 + c + k)
+    x, f = _u(rng, (n, c, h, w)), _u(rng, (k, c, r, s))
+    got, d = _run("conv2d", {"input": x, "filter": f}, (n, k, h - r + 1, w - s + 1))
+    assert d["conv_tf32"] == 1 and d["conv_generic"] == 0
+    sel = [0, n - 1]
+    ref = oracle.conv2d(x[sel], f).astype(np.float64)
+    _check(got[sel], ref, c * r * s)
+
+
+def test_conv2d_f32_channels_last():
+    rng = np.random.default_rng(4)
+    n, c, h, w, k = 2, 64, 20, 18, 96
+    x, f = _u(rng, (n, c, h, w)), _u(rng, (k, c, 3, 3))
+    xt = torch.from_numpy(x).to(DEV).contiguous(memory_format=torch.channels_last)
+    got, d = _run("conv2d", {"input": xt, "filter": f}, (n, k, h - 2, w - 2))
+    assert d["conv_tf32"] == 1
+    _check(got, oracle.conv2d(x, f).astype(np.float64), c * 9)
