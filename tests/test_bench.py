@@ -62,3 +62,16 @@ def test_compare_policy():
     assert ok["ok"] and ok["max_err"] == pytest.approx(0.01)
     bad = bench.compare([1.0, float("nan")], [1.0, 1.0], 1e-2, 1e-2)
     assert not bad["ok"]
+
+
+def test_tf32x3_roofline_and_fp32_tolerance():
+    # the 3xTF32 legs are judged against dense tf32 (half of bf16) / 3 MMAs
+    w = bench.Work("mm_f32", "tensor", 1, lambda n: 1e12 * n, None, None,
+                   peak_scale=bench.TF32X3_PEAK_SCALE)
+    r = bench._roofline(w, 1.0, {"hbm": 2000.0, "tc": 1200.0}, None)
+    assert r["peak"] == pytest.approx(200.0) and r["frac"] == pytest.approx(5.0)
+    assert "3xTF32" in r["peak_note"]
+    # the reference's 1e-4 (verify.py:24-25) at K <= 64, grown with sqrt(K)
+    assert bench.F32_MM_TOL(64) == (1e-5, 1e-4)
+    assert bench.F32_MM_TOL(4096)[1] == pytest.approx(8e-4)
+    assert all(k in bench.KERNELS for k in ("mm_f32", "bmm_f32", "conv2d_f32"))

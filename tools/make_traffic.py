@@ -1,0 +1,57 @@
+"""profiles/traffic.json from the ncu CSV of tools/traffic_probe.py: per bench
+key, the DRAM bytes of its launches, reads from dram__bytes_read and writes
+as max(dram__bytes_write, 32 B x lts__t_sectors_op_write) - writes still
+dirty in the 126 MB L2 when a kernel ends never reach DRAM inside the
+capture, so the L2 write sectors stand in for them.
+
+    python tools/make_traffic.py gpurun_out/r2_traffic.csv "softmax,rms_norm,..."
+"""
+import csv
+import io
+import json
+import sys
+from collections import defaultdict
+
+rows = [r for r in csv.reader(io.StringIO(open(sys.argv[1]).read())) if r]
+hdr = next(r for r in rows if "ID" in r and "Metric Name" in r)
+ix = {h: i for i, h in enumerate(hdr)}
+data = defaultdict(dict)
+names = {}
+for r in rows[rows.index(hdr) + 1:]:
+    if len(r) != len(hdr):
+        continue
+    lid = int(r[ix["ID"]])
+    names[lid] = r[ix["Kernel Name"]]
+    val = float(r[ix["Metric Value"]].replace(",", ""))
+    unit = r[ix["Metric Unit"]]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "sector": 1, "nsecond": 1,
+             "usecond": 1e3, "msecond": 1e6}.get(unit, 1)
+    data[lid][r[ix["Metric Name"]]] = val * scale
+order = sys.argv[2].split(",")
+# the launches of each key are those between consecutive synchronisations;
+# kernels are attributed by name: every key's main kernel families
+FAMILY = {"softmax": "row_stream", "rms_norm": "row_stream", "add_2^20": "ew_vec",
+          "add_2^24": "ew_vec", "silu_2^24": "ew_vec", "mm": "gemm_pair", "addmm": "gemm_pair",
+          "bmm": "gemm_pair", "mm_f32": "gemm_tf32", "bmm_f32": "gemm_tf32",
+          "conv2d": "conv_fused", "conv2d_f32": "gemm_tf32", "sdpa": "attn_fwd", "rope": "rope_vec",
+          "sdpa_rope": "attn_fwd"}
+ids = sorted(data)
+out, seen = {}, defaultdict(int)
+k = 0
+for key in order:
+    fam = FAMILY[key]
+    while k < len(ids) and fam not in names[ids[k]]:
+        k += 1
+    if k == len(ids):
+        break
+    d = data[ids[k]]
+    wr = max(d.get("dram__bytes_write.sum", 0), 32 * d.get("lts__t_sectors_op_write.sum", 0))
+    out[key] = int(d.get("dram__bytes_read.sum", 0) + wr)
+    k += 1
+out["_note"] = ("per launch, ncu on tools/traffic_probe.py (cold L2 per replay): "
+                "dram__bytes_read.sum + max(dram__bytes_write.sum, 32 B x lts__t_sectors_op_write.sum) "
+                "of the key's main kernel (writes left dirty in L2 at kernel end never reach DRAM "
+                "inside the capture; the L2 write sectors count them). sdpa_rope: the attention "
+                "kernel only (its K pre-pass is a separate rope_vec launch).")
+json.dump(out, open("profiles/traffic.json", "w"), indent=1)
+print(json.dumps(out, indent=1))
