@@ -70,6 +70,9 @@ struct TParams {
   int cb, pix_tiles, k_tiles, S, W, PW, Q, RS;
   float* y;
   int64_t ys[4];
+  // narrow tail (as the fp16 pair GEMM): units [n_whole, n_whole + 2 n_split)
+  // are the two 128-column halves of the last n_split tiles (N = 128 MMAs)
+  int n_whole, n_split;
 };
 
 __host__ __device__ constexpr uint32_t idesc_tf32(bool a_mn, bool b_mn, int M, int N) {
@@ -147,9 +150,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
   const uint32_t rank = cluster_rank();
   // GEMM tile t = (batch, n tile, m tile); conv tile t = (image, pixel tile, channel tile)
   const int tiles_per_batch = CONV ? p.pix_tiles * p.k_tiles : p.num_m * p.num_n;
-  const int total = tiles_per_batch * p.batch;
   const int nk = CONV ? p.RS * p.cb : (p.K + TBK - 1) / TBK;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int units = p.n_whole + 2 * p.n_split;
+  // unit -> tile t and column half hu (-1: the whole 256-column tile)
+  auto decode = [&](int u, int& t, int& hu) {
+    if (u < p.n_whole) {
+      t = u;
+      hu = -1;
+    } else {
+      t = p.n_whole + ((u - p.n_whole) >> 1);
+      hu = (u - p.n_whole) & 1;
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < T_STAGES; ++i) {
@@ -182,11 +195,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
     if (elect_one()) {
       int st = 0;
       uint32_t ph = 0;
-      for (int t = cid; t < total; t += ncl) {
+      for (int u = cid; u < units; u += ncl) {
+        int t, hu;
+        decode(u, t, hu);
         const int b = t / tiles_per_batch, r = t % tiles_per_batch;
         // conv: pixel tile = r / k_tiles ("n" role), channel tile = r % k_tiles ("m" role)
         const int nt = CONV ? r / p.k_tiles : r / p.num_m, mt = CONV ? r % p.k_tiles : r % p.num_m;
-        const int row = mt * 256 + (int)rank * 128, col = nt * 256 + (int)rank * 128;
+        // narrow units: each CTA supplies 64 of the 128 columns (the box still
+        // brings 128 rows; the N = 128 MMA reads the first 64)
+        const int row = mt * 256 + (int)rank * 128;
+        const int col = hu < 0 ? nt * 256 + (int)rank * 128 : nt * 256 + hu * 128 + (int)rank * 64;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[st], ph ^ 1);
           mbar_expect_tx(&full[st], 2 * T_TILE);
@@ -227,7 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
     // one cluster-scope release-arrive on CTA 0's "stage ready" barrier (the
     // release costs ~1k cycles, kept off the converters' path)
     int st = 0;
-    for (int t = cid; t < total; t += ncl)
+    for (int u = cid; u < units; u += ncl)
       for (int kb = 0; kb < nk; ++kb) {
         asm volatile("bar.sync %0, 96;" ::"r"(1 + st) : "memory");
         if (lane == 0) arrive_cluster_release(leader_addr(&ready[st]));
@@ -237,11 +255,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
     if (elect_one()) {
       // K chunks of T_CHUNK blocks alternate between the two TMEM buffers,
       // each starting from zero; the epilogue adds them in fp32 registers
-      constexpr uint32_t idesc = idesc_tf32(A_MN, B_MN, 256, 256);
+      constexpr uint32_t idesc_w = idesc_tf32(A_MN, B_MN, 256, 256);
+      constexpr uint32_t idesc_n = idesc_tf32(A_MN, B_MN, 256, 128);
       int st = 0;
       uint32_t ph = 0;
       int g = 0;   // chunk sequence number (buffer g & 1)
-      for (int t = cid; t < total; t += ncl) {
+      for (int u = cid; u < units; u += ncl) {
+        const uint32_t idesc = u < p.n_whole ? idesc_w : idesc_n;
         for (int kb = 0; kb < nk; ++kb) {
           if (kb % T_CHUNK == 0) {
             mbar_wait(&tempty[g & 1], ((g >> 1) & 1) ^ 1);
@@ -279,7 +299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
     const int ct = threadIdx.x - 64;
     int st = 0;
     uint32_t ph = 0;
-    for (int t = cid; t < total; t += ncl)
+    for (int u = cid; u < units; u += ncl)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&full[st], ph);
         const uint32_t raw = smem_u32(smem + st * T_STAGE);
@@ -327,16 +347,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
     uint8_t* stage = sC + (warp - 4) * (32 * 128);
     const int nchunks = (nk + T_CHUNK - 1) / T_CHUNK;
     int g = 0;
-    for (int t = cid; t < total; t += ncl) {
+    for (int u = cid; u < units; u += ncl) {
+      int t, hu;
+      decode(u, t, hu);
       const int b = t / tiles_per_batch, r = t % tiles_per_batch;
       const int nt = CONV ? r / p.k_tiles : r / p.num_m, mt = CONV ? r % p.k_tiles : r % p.num_m;
+      // this thread's columns: 128 of a whole tile, 64 of a narrow unit
+      const int nq = hu < 0 ? 4 : 2;   // 32-column chunks
+      const int cbase = hu < 0 ? nt * 256 + half * 128 : nt * 256 + hu * 128 + half * 64;
       float acc[128];
       for (int c = 0; c < nchunks; ++c, ++g) {
         mbar_wait(&tfull[g & 1], (g >> 1) & 1);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + (g & 1) * 256 + half * 128 + ((uint32_t)(quad * 32) << 16);
+        const uint32_t taddr = tmem_base + (g & 1) * 256 + half * (hu < 0 ? 128 : 64) +
+                               ((uint32_t)(quad * 32) << 16);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
+          if (q >= 2 * nq) break;
           uint32_t v[16];
           tmem_ld_32x32b_x16(taddr + q * 16, v);
           tmem_ld_wait();
@@ -354,12 +381,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
         // at col * 32 + (row + col) % 32: conflict-free both ways) so that a
         // warp's stores run along the output row of one channel
         const int k0 = mt * 256 + (int)rank * 128 + quad * 32;
-        const int pix0 = nt * 256 + half * 128;
+        const int pix0 = cbase;
         float* xp = reinterpret_cast<float*>(stage);
         const int kn = p.K - k0;
         float* ybase = p.y + (int64_t)b * p.ys[0] + (int64_t)k0 * p.ys[1];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
+          if (q >= nq) break;
           __syncwarp();
 #pragma unroll
           for (int i = 0; i < 32; ++i) xp[i * 32 + ((lane + i) & 31)] = acc[q * 32 + i];
@@ -387,7 +415,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
       const int row = row0 + lane;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int col0 = nt * 256 + half * 128 + q * 32;
+        if (q >= nq) break;
+        const int col0 = cbase + q * 32;
         float* f = acc + q * 32;
 #pragma unroll
         for (int i = 0; i < 32; ++i) f[i] *= p.alpha;
@@ -444,7 +473,7 @@ int launch_tf32(const TMaps& maps, const TParams& p, cudaStream_t s) {
   static size_t attr[kMaxDevices] = {};
   cudaError_t e = smem_attr_once(k, T_SMEM, attr);
   if (e != cudaSuccess) return cuda_fail(e, "gemm tf32 smem attribute");
-  const int total = (CONV ? p.pix_tiles * p.k_tiles : p.num_m * p.num_n) * p.batch;
+  const int total = p.n_whole + p.n_split;
   int clusters = sm_count() / 2;
   if (total < clusters) clusters = total;
   e = launch_pdl(k, dim3(2 * clusters), dim3(T_THREADS), T_SMEM, s, maps, p);
@@ -454,6 +483,16 @@ int launch_tf32(const TMaps& maps, const TParams& p, cudaStream_t s) {
 }
 
 bool ok_stride4(int64_t elems) { return elems > 0 && (elems * 4) % 16 == 0; }
+
+// narrow tail: if the last wave would leave more than half of the CTA pairs
+// idle, its tiles run as two 256 x 128 units each (NTB_GEMM_NO_SPLIT=1: off)
+void set_tail(TParams& p, int64_t total) {
+  const int64_t pairs = sm_count() / 2;
+  const int64_t rem = total % pairs;
+  static const bool split = !getenv("NTB_GEMM_NO_SPLIT");
+  p.n_split = (split && total > pairs && rem > 0 && 2 * rem <= pairs) ? (int)rem : 0;
+  p.n_whole = (int)(total - p.n_split);
+}
 
 }  // namespace
 
@@ -519,6 +558,7 @@ int gemm_tf32_sm100(const GemmDesc& g, cudaStream_t s) {
   p.alpha = g.alpha;
   p.beta = g.beta;
   p.has_d = g.d != nullptr;
+  set_tail(p, (int64_t)p.num_m * p.num_n * p.batch);
   static const int passes = [] {
     const char* e = getenv("NTB_TF32_PASSES");
     return e && e[0] == '1' ? 1 : 3;
@@ -638,6 +678,7 @@ int conv_tf32_sm100(const ConvDesc& c, cudaStream_t s) {
   p.alpha = 1.f;
   p.y = static_cast<float*>(c.y);
   for (int d = 0; d < 4; ++d) p.ys[d] = c.ys[d];
+  set_tail(p, (int64_t)p.pix_tiles * p.k_tiles * p.batch);
   static const int passes = [] {
     const char* e = getenv("NTB_TF32_PASSES");
     return e && e[0] == '1' ? 1 : 3;

@@ -164,3 +164,38 @@ def test_conv2d_f32_channels_last():
     got, d = _run("conv2d", {"input": xt, "filter": f}, (n, k, h - 2, w - 2))
     assert d["conv_tf32"] == 1
     _check(got, oracle.conv2d(x, f).astype(np.float64), c * 9)
+
+
+@pytest.mark.parametrize("kernel,shape", [("mm", (2560, 4096, 1024)), ("addmm", (2560, 4096, 512)),
+                                          ("bmm", (3, 1536, 1280, 512)),
+                                          ("conv2d", (7, 64, 56, 56, 256, 3, 3))])
+def test_f32_narrow_tail(kernel, shape):
+    """Tile counts that leave the last wave of the 74 CTA pairs less than half
+    full (160, 90, 84 tiles) run the tail tiles as two 256 x 128 units; every
+    output element is checked."""
+    rng = np.random.default_rng(sum(shape))
+    if kernel == "conv2d":
+        n, c, h, w, k, r, s = shape
+        x, f = _u(rng, (n, c, h, w)), _u(rng, (k, c, r, s))
+        got, d = _run("conv2d", {"input": x, "filter": f}, (n, k, h - r + 1, w - s + 1))
+        assert d["conv_tf32"] == 1
+        _check(got, oracle.conv2d(x, f).astype(np.float64), c * r * s)
+        return
+    if kernel == "bmm":
+        bt, m, n, k = shape
+        a, b = _u(rng, (bt, m, k)), _u(rng, (bt, k, n))
+        got, d = _run("bmm", {"input": a, "other": b}, (bt, m, n))
+        ref = oracle.bmm(a, b)
+    else:
+        m, n, k = shape
+        a, b = _u(rng, (m, k)), _u(rng, (k, n))
+        if kernel == "mm":
+            got, d = _run("mm", {"input": a, "other": b}, (m, n))
+            ref = oracle.mm(a, b)
+        else:
+            inp = _u(rng, (m, n))
+            got, d = _run("addmm", {"input": inp, "mat1": a, "mat2": b, "beta": 0.5, "alpha": -1.5},
+                          (m, n))
+            ref = oracle.addmm(inp, a, b, 0.5, -1.5)
+    assert d["gemm_tf32"] == 1
+    _check(got, ref.astype(np.float64), k)

@@ -1,6 +1,6 @@
 """profiles/traffic.json from the ncu CSV of tools/traffic_probe.py: per bench
 key, the DRAM bytes of its launches, reads from dram__bytes_read and writes
-as max(dram__bytes_write, 32 B x lts__t_sectors_op_write) - writes still
+as max(dram__bytes_write, 32 B x lts__t_sectors_srcunit_tex_op_write) - writes still
 dirty in the 126 MB L2 when a kernel ends never reach DRAM inside the
 capture, so the L2 write sectors stand in for them.
 
@@ -45,11 +45,11 @@ for key in order:
     if k == len(ids):
         break
     d = data[ids[k]]
-    wr = max(d.get("dram__bytes_write.sum", 0), 32 * d.get("lts__t_sectors_op_write.sum", 0))
+    wr = max(d.get("dram__bytes_write.sum", 0), 32 * d.get("lts__t_sectors_srcunit_tex_op_write.sum", 0))
     out[key] = int(d.get("dram__bytes_read.sum", 0) + wr)
     k += 1
 out["_note"] = ("per launch, ncu on tools/traffic_probe.py (cold L2 per replay): "
-                "dram__bytes_read.sum + max(dram__bytes_write.sum, 32 B x lts__t_sectors_op_write.sum) "
+                "dram__bytes_read.sum + max(dram__bytes_write.sum, 32 B x lts__t_sectors_srcunit_tex_op_write.sum) "
                 "of the key's main kernel (writes left dirty in L2 at kernel end never reach DRAM "
                 "inside the capture; the L2 write sectors count them). sdpa_rope: the attention "
                 "kernel only (its K pre-pass is a separate rope_vec launch).")

@@ -1,7 +1,7 @@
 #!/bin/bash
 # round-2 final evidence pass (GPU box via gpurun; 1 GPU)
 mkdir -p gpurun_out
-M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_op_write.sum"
+M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_write.sum"
 N="ncu --set full --clock-control none --import-source on"
 timeout 600 python bench.py > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r2_ref.json 2> gpurun_out/r2_ref.err

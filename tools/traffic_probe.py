@@ -1,7 +1,7 @@
 """One launch of every bench kernel at its BASELINE shape (eager, through
 the public launchers), in a fixed order, for ncu metric collection:
 
-    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_op_write.sum,\
+    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_write.sum,\
 gpu__time_duration.sum --clock-control none --csv --log-file X python tools/traffic_probe.py
 
 tools/make_traffic.py turns the CSV into profiles/traffic.json."""
