@@ -85,7 +85,8 @@ enum {
   NTB_PATH_JIT = 15,
   NTB_PATH_GEMM_TF32 = 16,  /* fp32 mm/bmm/addmm: 3xTF32 on tcgen05 */
   NTB_PATH_CONV_TF32 = 17,  /* fp32 conv2d: 3xTF32 implicit GEMM on tcgen05 */
-  NTB_NUM_PATHS = 18
+  NTB_PATH_EW_STREAM = 18,  /* add / silu: bulk-copy (TMA) streaming kernel */
+  NTB_NUM_PATHS = 19
 };
 int64_t ntb_path_count(int path);
 

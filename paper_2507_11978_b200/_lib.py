@@ -119,7 +119,7 @@ def map_enumerate(blob: np.ndarray, param: int, slots: np.ndarray):
 
 PATHS = ("probe", "ew_vec", "ew_generic", "row_vec", "row_generic", "rope_vec", "rope_generic",
          "gemm_tc", "gemm_generic", "conv_tc", "conv_generic", "attn_tc", "attn_generic", "repack", "row_stream", "jit",
-         "gemm_tf32", "conv_tf32")
+         "gemm_tf32", "conv_tf32", "ew_stream")
 
 
 def path_counts() -> dict:

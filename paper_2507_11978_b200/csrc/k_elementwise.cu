@@ -10,6 +10,8 @@
 // launch is a grid-stride loop of 128-bit vectors sized to the SM count.
 //
 // HBM roofline: add moves 3 x n x sizeof(T) bytes, silu 2 x n x sizeof(T).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 #ifndef NTB_EW_UNROLL
@@ -18,13 +20,61 @@
 
 namespace ntb {
 
+// Each op maps a pack of n fp32 values in place (b: the second input).
 struct AddOp {
   static constexpr int kIn = 2;
-  __device__ __forceinline__ float operator()(float a, float b) const { return a + b; }
+  template <int n>
+  __device__ __forceinline__ void apply(float (&a)[n], const float (&b)[n]) const {
+#pragma unroll
+    for (int e = 0; e < n; ++e) a[e] += b[e];
+  }
 };
+// silu(x) = x / (1 + 2^(-x log2 e)).  Two elements share one reciprocal:
+// 1/d0 = d1 / (d0 d1) and 1/d1 = d0 / (d0 d1) while d0 d1 < 2^126 (both
+// reciprocals then stay normal fp32); otherwise (x < -43 in one of the two,
+// or a NaN) each gets its own.  3 SFU ops per pair instead of 4: at 2^24
+// 16-bit elements, 2 SFU ops per element are 7.4 us of SFU time per SMSP
+// against 10.3 us of HBM time.
 struct SiluOp {
   static constexpr int kIn = 1;
-  __device__ __forceinline__ float operator()(float x, float) const {
+  static __device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  }
+  static __device__ __forceinline__ float rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  }
+  template <int n>
+  __device__ __forceinline__ void apply(float (&x)[n], const float (&)[n]) const {
+    static_assert(n % 2 == 0, "pairs");
+#if NTB_SILU_CHEAP
+#pragma unroll
+    for (int e = 0; e < n; ++e) x[e] *= 0.5f;
+    return;
+#endif
+#pragma unroll
+    for (int e = 0; e < n; e += 2) {
+      const float d0 = 1.0f + ex2(-x[e] * 1.4426950408889634f);
+      const float d1 = 1.0f + ex2(-x[e + 1] * 1.4426950408889634f);
+      const float pr = d0 * d1;
+      float s0, s1;
+      if (pr < 0x1p126f) {
+        const float r = rcp(pr);
+        s0 = d1 * r;
+        s1 = d0 * r;
+      } else {
+        s0 = rcp(d0);
+        s1 = rcp(d1);
+      }
+      x[e] *= s0;
+      x[e + 1] *= s1;
+    }
+  }
+  // one element (generic strided path)
+  __device__ __forceinline__ float one(float x) const {
     return __fdividef(x, 1.0f + exp2f(-x * 1.4426950408889634f));
   }
 };
@@ -70,13 +120,138 @@ __global__ void __launch_bounds__(256) ew_vec_kernel(const T* __restrict__ a,
       float fa[P::N], fb[P::N];
       va[u].to_float(fa);
       if (Op::kIn == 2) vb[u].to_float(fb);
-#pragma unroll
-      for (int k = 0; k < P::N; ++k) fa[k] = op(fa[k], Op::kIn == 2 ? fb[k] : 0.f);
+      op.apply(fa, fb);
       P r;
       r.from_float(fa);
       st_stream(out + (i + u * stride) * P::N, r.raw);
     }
   }
+}
+
+// ---- TMA-bulk streaming path ------------------------------------------------
+// Persistent CTAs (one per SM) of 16 warps.  The array is cut into chunks of
+// 32 x VPL 16-byte packs per input; chunk c belongs to warp (c mod G) of the
+// grid-interleaved warp order (G = grid x 16 warps), as rows are in the
+// row-streaming kernel.  Each warp owns a ring of STAGES shared-memory slots
+// (one buffer per input), each filled by one cp.async.bulk per input with
+// completion on the slot's mbarrier; the warp moves a chunk to registers,
+// requests the chunk STAGES ahead into the same slot right away, then
+// computes and writes it with 128-bit streaming stores - no per-thread load
+// queue.  The first chunks of every warp are requested into L2 before the
+// PDL wait.  Measured (silu fp16 2^24, B200): 2 KB chunks, one slot, 16
+// warps: 12.6 us; 8 KB chunks 14.4 us (the SFU work of a chunk then runs
+// in one burst per warp); 2-4 slots or 32 warps 12.9-14.5 us.
+#ifndef NTB_EW_WARPS
+#define NTB_EW_WARPS 16
+#endif
+#ifndef NTB_EW_STAGES
+#define NTB_EW_STAGES 1
+#endif
+#ifndef NTB_EW_VPL1
+#define NTB_EW_VPL1 4
+#endif
+constexpr int kEwWarps = NTB_EW_WARPS;
+
+template <typename T, typename Op, int VPL, int kEwStages>
+__global__ void __launch_bounds__(kEwWarps * 32, 1)
+    ew_stream_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out,
+                     int64_t n_vec) {
+  using P = Pack<T>;
+  constexpr int CH = 32 * VPL;                // packs per chunk
+  constexpr uint32_t CH_BYTES = CH * 16;
+  constexpr uint32_t SLOT = Op::kIn * CH_BYTES;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[kEwWarps][kEwStages];
+  Op op;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + (size_t)warp * kEwStages * SLOT;
+  const int64_t n_chunks = (n_vec + CH - 1) / CH;
+  const int64_t step = (int64_t)gridDim.x * kEwWarps;
+  const int64_t first = (int64_t)blockIdx.x + (int64_t)gridDim.x * warp;
+  auto chunk_bytes = [&](int64_t c) -> uint32_t {
+    const int64_t v = n_vec - c * CH;
+    return (uint32_t)((v < CH ? v : CH) * 16);
+  };
+  auto request = [&](int64_t c, int s) {
+    const uint32_t nb = chunk_bytes(c);
+    uint8_t* buf = ring + s * SLOT;
+    bar_expect(&bars[warp][s], nb * Op::kIn);
+    bulk_g2s(buf, a + c * CH * P::N, nb, &bars[warp][s]);
+    if (Op::kIn == 2) bulk_g2s(buf + CH_BYTES, b + c * CH * P::N, nb, &bars[warp][s]);
+  };
+#if !NTB_EW_NO_PREFETCH
+  if (lane < kEwStages * Op::kIn) {
+    const int64_t c = first + (lane / Op::kIn) * step;
+    if (c < n_chunks) prefetch_l2_bulk(((lane % Op::kIn) ? b : a) + c * CH * P::N, chunk_bytes(c));
+  }
+#endif
+  pdl_wait();
+  pdl_trigger();
+  if (lane == 0) {
+    for (int s = 0; s < kEwStages; ++s) bar_init(&bars[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < kEwStages; ++s)
+      if (first + s * step < n_chunks) request(first + s * step, s);
+  }
+  __syncwarp();
+  int64_t k = 0;
+  for (int64_t c = first; c < n_chunks; c += step, ++k) {
+    const int s = (int)(k % kEwStages);
+    bar_wait(&bars[warp][s], (uint32_t)((k / kEwStages) & 1));
+    const uint4* sa = reinterpret_cast<const uint4*>(ring + s * SLOT);
+    const uint4* sb = reinterpret_cast<const uint4*>(ring + s * SLOT + CH_BYTES);
+    const int64_t v0 = c * CH;
+    const int nv = (int)(n_vec - v0 < CH ? n_vec - v0 : CH);
+    P va[VPL], vb[VPL];
+#pragma unroll
+    for (int u = 0; u < VPL; ++u) {
+      const int i = lane + 32 * u;
+      if (i < nv) {
+        va[u].raw = sa[i];
+        if (Op::kIn == 2) vb[u].raw = sb[i];
+      }
+    }
+    // all lanes have read the buffer: refill it with the warp's chunk S ahead
+    __syncwarp();
+    if (lane == 0 && c + kEwStages * step < n_chunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      request(c + kEwStages * step, s);
+    }
+#pragma unroll
+    for (int u = 0; u < VPL; ++u) {
+      const int i = lane + 32 * u;
+      if (i >= nv) break;
+      float fa[P::N], fb[P::N];
+      va[u].to_float(fa);
+      if (Op::kIn == 2) vb[u].to_float(fb);
+      op.apply(fa, fb);
+      P r;
+      r.from_float(fa);
+      st_stream(out + (v0 + i) * P::N, r.raw);
+    }
+  }
+}
+
+// Launch the streaming path; false if its shared memory cannot be granted.
+template <typename T, typename Op>
+static bool try_ew_stream(const T* a, const T* b, T* out, int64_t n_vec, cudaStream_t s) {
+  constexpr int VPL = Op::kIn == 1 ? NTB_EW_VPL1 : 8;
+  constexpr int64_t CH = 32 * VPL;
+  // ring depth: the configured one, capped at 192 KB of buffers per CTA
+  constexpr int64_t kMaxStages = (192 * 1024) / (kEwWarps * Op::kIn * CH * 16);
+  constexpr int STAGES = NTB_EW_STAGES < kMaxStages ? NTB_EW_STAGES : (kMaxStages > 0 ? kMaxStages : 1);
+  const size_t smem = (size_t)kEwWarps * STAGES * Op::kIn * CH * 16;
+  auto kern = ew_stream_kernel<T, Op, VPL, STAGES>;
+  static size_t attr[kMaxDevices] = {};
+  if (smem_attr_once(kern, smem, attr) != cudaSuccess) {
+    cudaGetLastError();   // not sticky: the caller falls back to the register-queue kernel
+    return false;
+  }
+  const int64_t n_chunks = cdiv64(n_vec, CH);
+  int64_t blocks = cdiv64(n_chunks, kEwWarps);
+  if (blocks > sm_count()) blocks = sm_count();
+  return launch_pdl(kern, dim3((unsigned)blocks), dim3(kEwWarps * 32), smem, s, a, b, out,
+                    n_vec) == cudaSuccess;
 }
 
 // Generic path: any element strides / mismatched sizes / unaligned bases.
@@ -88,7 +263,10 @@ __global__ void ew_generic_kernel(const T* a, int64_t na, int64_t sa, const T* b
        i += (int64_t)gridDim.x * blockDim.x) {
     float x = i < na ? Elem<T>::to_f(a[i * sa]) : 0.f;
     float y = (Op::kIn == 2 && i < nb) ? Elem<T>::to_f(b[i * sb]) : 0.f;
-    out[i * so] = Elem<T>::from_f(op(x, y));
+    float r;
+    if constexpr (Op::kIn == 2) r = x + y;
+    else r = op.one(x);
+    out[i * so] = Elem<T>::from_f(r);
   }
 }
 
@@ -108,6 +286,19 @@ static int run_ew(const LaunchArgs& A) {
   const int sms = sm_count();
   if (fast) {
     int64_t n_vec = no / N;
+    // path choice (measured): the bulk-copy streaming
+    // kernel once a launch moves >= 32 MB (silu fp16 2^24: 0.74-0.79 -> 0.81
+    // of HBM, add fp32 2^24: 0.97 -> 1.01); below that the register-queue
+    // kernel, whose first wave is one L2-prefetched round trip (add fp32
+    // 2^20: 3.1-3.3 us vs 3.5-3.6 streaming).  NTB_EW_PATH=vec|stream forces one.
+    static const int forced = [] {
+      const char* e = getenv("NTB_EW_PATH");
+      return !e ? 0 : (e[0] == 's' ? 2 : 1);
+    }();
+    const int64_t bytes = no * (int64_t)sizeof(T) * (nin + 1);
+    const bool stream = forced ? forced == 2 : bytes >= (32ll << 20);
+    if (stream && try_ew_stream<T, Op>(a, b, out, n_vec, A.stream))
+      return check_launch("elementwise stream", NTB_PATH_EW_STREAM);
     // one wave of 8 resident 256-thread CTAs per SM, each thread U vectors
     // per input in flight per iteration (measured: 8 for fp32 add 2^24 =
     // 0.97 of HBM, 4 for the 16-bit silu 2^24 = 0.80)

@@ -124,7 +124,9 @@ DTS = [torch.float16, torch.bfloat16]
 
 
 @pytest.mark.parametrize("dtype", DTS)
-@pytest.mark.parametrize("n", [1, 37, 4096, 1 << 20])
+# 8000: a partial last chunk in the streaming kernel; the last size gives
+# every warp of a 148-SM grid two full chunks and a ragged third
+@pytest.mark.parametrize("n", [1, 37, 4096, 8000, 1 << 20, 8 * (512 * 148 * 16 * 2 + 77)])
 def test_elementwise_half(dtype, n):
     rng = np.random.default_rng(n)
     a, b = (_r16(rng.uniform(-1, 1, n).astype(np.float32), dtype) for _ in range(2))
@@ -132,6 +134,43 @@ def test_elementwise_half(dtype, n):
     _close(got, oracle.add(a, b), rtol=1e-2, atol=1e-3)
     got = _run("silu", {"input": a}, {"BLOCK_SIZE": 1024}, dtype)
     _close(got, oracle.silu(a), rtol=1e-2, atol=1e-3)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float16, torch.bfloat16])
+def test_silu_magnitude_sweep(dtype):
+    """silu pairs two elements on one reciprocal while d0*d1 < 2^126 and falls
+    back to one reciprocal each beyond (k_elementwise.cu SiluOp): inputs from
+    1e-3 to 1e4 in magnitude, both signs, so pairs straddle the fallback
+    (x < -43), plus exact zeros and a ragged tail."""
+    rng = np.random.default_rng(11)
+    parts = [rng.normal(0, s, 4096) for s in (1e-3, 0.1, 1.0, 10.0, 30.0, 100.0, 1e4)]
+    x = np.concatenate(parts + [np.zeros(64), np.array([-43.0, -44.0, -90.0, 88.0, -1e30, 1e30])])
+    x = rng.permutation(x.astype(np.float32))
+    if dtype != torch.float32:
+        x = np.clip(x, -6e4, 6e4) if dtype == torch.float16 else x
+        x = _r16(x, dtype)
+    before = backend.path_counts()
+    for n in ((x.size // 8) * 8, (x.size // 8) * 8 - 3):   # vector path, then the strided one
+        got = _run("silu", {"input": x[:n]}, {"BLOCK_SIZE": 1024}, dtype)
+        ref = oracle.silu(x[:n]).astype(np.float64)
+        if dtype == torch.float32:
+            _close(got, ref, rtol=1e-5, atol=1e-30)
+        else:
+            _close(got, ref, rtol=1e-2, atol=1e-3)
+    d = {k: v - before.get(k, 0) for k, v in backend.path_counts().items()}
+    assert d["ew_generic"] == 1 and d["ew_vec"] + d["ew_stream"] == 1, d
+
+
+@pytest.mark.parametrize("n", [(1 << 24), (1 << 24) + 4 * 77])
+def test_add_fp32_streaming_bit_exact(n):
+    """>= 32 MB per launch takes the bulk-copy streaming kernel (ew_stream):
+    still byte-identical to the oracle / sim (fp32 a + b, one rounding)."""
+    rng = np.random.default_rng(n)
+    a, b = (rng.uniform(-1, 1, n).astype(np.float32) for _ in range(2))
+    with _Paths() as pc:
+        got = _run("add", {"input": a, "other": b}, {"BLOCK_SIZE": 1024}).cpu().numpy()
+    assert pc.delta["ew_stream"] == 1, pc.delta
+    assert got.tobytes() == oracle.add(a, b).tobytes()
 
 
 def test_add_fp32_large_bit_exact():
