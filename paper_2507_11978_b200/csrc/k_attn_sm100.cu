@@ -81,6 +81,11 @@ struct AttnMaps {
 
 struct AttnParams {
   int B, H, Sq, Sk, n_qt, n_items;
+  // work units: items [0, n_full) round-robin over the grid, then (when the
+  // last round would leave more than half of the CTAs idle) the remaining
+  // items as 2 * (n_items - n_full) = n_half SINGLE-TILE units, unit
+  // n_full + u on CTA u: query tile u % 2 of item n_full + u / 2
+  int n_full, n_half;
   float scale_log2;
   void* o;
   int64_t os[4];
@@ -223,6 +228,25 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return BF16 ? sm100::pack_bf16(a, b) : sm100::pack_f16(a, b);
 }
 
+// The CTA's it-th work unit: item and query tile (-1: both tiles, the
+// ping-pong; 0 / 1: that tile alone, on softmax warpgroup 0 and TMEM S0/O0).
+// A single-tile unit is always the CTA's last.
+__device__ __forceinline__ int n_units(const AttnParams& p) {
+  const int b = (int)blockIdx.x, g = (int)gridDim.x;
+  return (b < p.n_full ? (p.n_full - b + g - 1) / g : 0) + (b < p.n_half ? 1 : 0);
+}
+__device__ __forceinline__ void unit_of(const AttnParams& p, int it, int& item, int& half) {
+  const int b = (int)blockIdx.x, g = (int)gridDim.x;
+  const int nf = b < p.n_full ? (p.n_full - b + g - 1) / g : 0;
+  if (it < nf) {
+    item = b + it * g;
+    half = -1;
+  } else {
+    item = p.n_full + b / 2;
+    half = b & 1;
+  }
+}
+
 template <int D, bool BF16, bool ROPE>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_kernel(const __grid_constant__ AttnMaps maps, const AttnParams p) {
@@ -275,25 +299,32 @@ __global__ void __launch_bounds__(384, 1)
       tma_prefetch(&maps.k);
       tma_prefetch(&maps.v);
       uint32_t c = 0;  // K/V ring sequence number: K_j, V_j, K_{j+1}, ...
-      auto load_q = [&](int item, int it) {
+      const int nu = n_units(p);
+      auto load_q = [&](int it) {
+        int item, half;
+        unit_of(p, it, item, half);
         const int qt = item % p.n_qt, bh = item / p.n_qt, h = bh % p.H, b = bh / p.H;
         const int qb = it % L::QB;
         mbar_wait(&q_empty[qb], ((it / L::QB) & 1) ^ 1);
-        mbar_expect_tx(&q_full[qb], 2 * L::Q_BYTES);
+        mbar_expect_tx(&q_full[qb], (half < 0 ? 2 : 1) * L::Q_BYTES);
 #pragma unroll
-        for (int g = 0; g < 2; ++g)
+        for (int g = 0; g < 2; ++g) {
+          if (half >= 0 && g == 1) break;
+          const int tile = half < 0 ? g : half;   // a single tile goes to slot 0
 #pragma unroll
           for (int ch = 0; ch < L::DCH; ++ch)
             tma_load_4d(smem + L::OFF_Q + (qb * 2 + g) * L::Q_BYTES + ch * (BM * 128), &maps.q,
-                        &q_full[qb], ch * 64, qt * 2 * BM + g * BM, h, b);
+                        &q_full[qb], ch * 64, qt * 2 * BM + tile * BM, h, b);
+        }
       };
-      // two Q buffers: the next item's Q is requested before this item's K/V
-      if (L::QB == 2 && (int)blockIdx.x < p.n_items) load_q(blockIdx.x, 0);
-      int it = 0;
-      for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+      // two Q buffers: the next unit's Q is requested before this unit's K/V
+      if (L::QB == 2 && nu > 0) load_q(0);
+      for (int it = 0; it < nu; ++it) {
+        int item, half;
+        unit_of(p, it, item, half);
         const int bh = item / p.n_qt, h = bh % p.H, b = bh / p.H;
-        if (L::QB == 1) load_q(item, it);
-        else if (item + (int)gridDim.x < p.n_items) load_q(item + gridDim.x, it + 1);
+        if (L::QB == 1) load_q(it);
+        else if (it + 1 < nu) load_q(it + 1);
         for (int j = 0; j < n_kv; ++j) {
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv, ++c) {
@@ -347,25 +378,39 @@ __global__ void __launch_bounds__(384, 1)
                      !(first && kk == 0));
         }
       };
-      for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+      const int nu = n_units(p);
+      for (it = 0; it < nu; ++it) {
+        int item, half;
+        unit_of(p, it, item, half);
+        (void)item;
+        // two: the ping-pong of both query tiles; otherwise tile 0 alone, and
+        // the K / V / Q buffers are released after its own MMAs
+        const bool two = half < 0;
         qb = it % L::QB;
         mbar_wait(ROPE ? &q_rot[qb] : &q_full[qb], (it / L::QB) & 1);
         tc_fence_after();
         wait_kv(c);
         issue_s(0, c);
-        issue_s(1, c);
+        if (two) issue_s(1, c);
         mma_commit(&kv_empty[c % L::NS]);
         if (n_kv == 1) mma_commit(&q_empty[qb]);
         for (int j = 0; j < n_kv; ++j, ++t) {
           const bool more = j + 1 < n_kv;
           const uint32_t kseq = c + 2 * j, vseq = kseq + 1, knext = kseq + 2;
+          auto next_s0 = [&]() {
+            issue_s(0, knext);
+            if (!two) {
+              mma_commit(&kv_empty[knext % L::NS]);
+              if (j + 2 == n_kv) mma_commit(&q_empty[qb]);
+            }
+          };
           // ---- query tile 0
           TRACE_MMA(j, 0)
           if (L::SEP_P && more) {
             // S_0 columns already read by the softmax: next S right away
             mbar_wait(&s_free[0], t & 1);
             wait_kv(knext);
-            issue_s(0, knext);
+            next_s0();
           }
           mbar_wait(&p_full[0][0], t & 1);
           tc_fence_after();
@@ -383,16 +428,18 @@ __global__ void __launch_bounds__(384, 1)
             issue_pv(0, vseq, j == 0, q);
           }
           TRACE_MMA(j, 2)
+          if (!two) mma_commit(&kv_empty[vseq % L::NS]);
           if (L::SEP_P) mma_commit(&pv_done[0]);
           if (more) {
             if (!L::SEP_P) {
               wait_kv(knext);
               TRACE_MMA(j, 3)
-              issue_s(0, knext);
+              next_s0();
             }
           } else {
             mma_commit(&o_full[0]);
           }
+          if (!two) continue;
           // ---- query tile 1
           TRACE_MMA(j, 4)
           if (L::SEP_P && more) {
@@ -438,14 +485,17 @@ __global__ void __launch_bounds__(384, 1)
     // 7.2 ms, because the 16 query blocks that share a K tile each redo it
     // and the table reads double the L2 stream.)
     const int t = (warp - 2) * 32 + lane;
-    int it = 0;
-    for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+    const int nu = n_units(p);
+    for (int it = 0; it < nu; ++it) {
+      int item, half;
+      unit_of(p, it, item, half);
       const int qt = item % p.n_qt, qb = it % L::QB;
       mbar_wait(&q_full[qb], (it / L::QB) & 1);
 #pragma unroll 1
-      for (int g = 0; g < 2; ++g)
+      for (int g = 0; g < (half < 0 ? 2 : 1); ++g)
         rope_tile<D, BF16>(smem + L::OFF_Q + (qb * 2 + g) * L::Q_BYTES, BM * 128, BM,
-                           qt * 2 * BM + g * BM, p.Sq, p.sin_q, p.sq_rs, p.cos_q, p.cq_rs, t, 64);
+                           qt * 2 * BM + (half < 0 ? g : half) * BM, p.Sq, p.sin_q, p.sq_rs,
+                           p.cos_q, p.cq_rs, t, 64);
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_rot[qb]);
@@ -462,8 +512,13 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t t_o = tmem + (g ? L::T_O1 : L::T_O0) + lane_off;
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     uint32_t t = 0;
-    int it = 0;
-    for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+    const int nu = n_units(p);
+    for (int it = 0; it < nu; ++it) {
+      int item, half;
+      unit_of(p, it, item, half);
+      // a single-tile unit (always the last) runs on warpgroup 0 alone
+      if (half >= 0 && g == 1) break;
+      const int tile = half < 0 ? g : half;
       const int qt = item % p.n_qt, bh = item / p.n_qt, h = bh % p.H, b = bh / p.H;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_kv; ++j, ++t) {
@@ -587,7 +642,7 @@ __global__ void __launch_bounds__(384, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[g]);
       const float inv = 1.f / l;
-      const int qrow = qt * 2 * BM + g * BM + row;
+      const int qrow = qt * 2 * BM + tile * BM + row;
       if (qrow < p.Sq) {
         char* obase = reinterpret_cast<char*>(p.o) +
                       ((int64_t)b * p.os[0] + (int64_t)h * p.os[1] + (int64_t)qrow * p.os[2]) * 2;
@@ -624,13 +679,36 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 template <int D, bool BF16, bool ROPE>
-int launch_attn(const AttnMaps& maps, const AttnParams& p, cudaStream_t s) {
+int launch_attn(const AttnMaps& maps, AttnParams p, cudaStream_t s) {
   using L = Layout<D, ROPE>;
   auto k = attn_fwd_kernel<D, BF16, ROPE>;
   static size_t attr[kMaxDevices] = {};
   cudaError_t e = smem_attr_once(k, L::SMEM, attr);
   if (e != cudaSuccess) return cuda_fail(e, "attention smem attribute");
-  const int grid = p.n_items < sm_count() ? p.n_items : sm_count();
+  // Tail split: when the last round of items would leave more than half of
+  // the CTAs idle, its items run as two single-tile units each on twice as
+  // many CTAs (a single-tile unit takes ~half to ~3/4 of an item: the chain
+  // of one warpgroup instead of the ping-pong of two).  Small problems
+  // (<= SMs / 2 items) run entirely as single-tile units.
+  static const bool split = !getenv("NTB_ATTN_NO_SPLIT");
+  const int sms = sm_count();
+  int grid = p.n_items < sms ? p.n_items : sms;
+  p.n_full = p.n_items;
+  p.n_half = 0;
+  if (split) {
+    if (2 * p.n_items <= sms) {
+      p.n_full = 0;
+      p.n_half = 2 * p.n_items;
+      grid = p.n_half;
+    } else {
+      const int rounds = (p.n_items + grid - 1) / grid;
+      const int tail = p.n_items - (rounds - 1) * grid;
+      if (rounds > 1 && 2 * tail <= grid) {
+        p.n_full = (rounds - 1) * grid;
+        p.n_half = 2 * tail;
+      }
+    }
+  }
   k<<<grid, 384, L::SMEM, s>>>(maps, p);
 #if NTB_ATTN_TRACE
   {

@@ -35,6 +35,13 @@ struct AddOp {
 // or a NaN) each gets its own.  3 SFU ops per pair instead of 4: at 2^24
 // 16-bit elements, 2 SFU ops per element are 7.4 us of SFU time per SMSP
 // against 10.3 us of HBM time.
+#ifndef NTB_SILU_FMA_EVERY
+// 16-bit outputs: every k-th pair's 2^t on the FMA pipe (0: all on the SFU).
+// fp32 outputs always use the SFU (the cubic's 7.5e-5 is above fp32's 1e-5
+// silu tolerance).  Measured silu fp16 2^24: k = 2 12.2-12.3 us, SFU only
+// 12.4-12.7 us.
+#define NTB_SILU_FMA_EVERY 2
+#endif
 struct SiluOp {
   static constexpr int kIn = 1;
   static __device__ __forceinline__ float ex2(float x) {
@@ -47,18 +54,39 @@ struct SiluOp {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
   }
+  // 2^t for a pair on the FMA pipe: t clamped to [-125, 127], t = i + f with
+  // i = rint(t) (1.5 * 2^23 trick), 2^f by a cubic (rel. err 7.5e-5, below
+  // half an fp16 / bf16 ulp), 2^i added into the exponent field
+  static __device__ __forceinline__ float2 ex2_fma(float2 t) {
+    t.x = fminf(fmaxf(t.x, -125.f), 127.f);
+    t.y = fminf(fmaxf(t.y, -125.f), 127.f);
+    const float2 m = __fadd2_rn(t, make_float2(12582912.0f, 12582912.0f));
+    const float2 r = __fadd2_rn(m, make_float2(-12582912.0f, -12582912.0f));
+    const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), t);
+    float2 q = __ffma2_rn(f, make_float2(0.0551702793f, 0.0551702793f),
+                          make_float2(0.242607975f, 0.242607975f));
+    q = __ffma2_rn(q, f, make_float2(0.693260928f, 0.693260928f));
+    q = __ffma2_rn(q, f, make_float2(0.999928276f, 0.999928276f));
+    return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(m.x) << 23)),
+                       __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(m.y) << 23)));
+  }
   template <int n>
   __device__ __forceinline__ void apply(float (&x)[n], const float (&)[n]) const {
     static_assert(n % 2 == 0, "pairs");
-#if NTB_SILU_CHEAP
-#pragma unroll
-    for (int e = 0; e < n; ++e) x[e] *= 0.5f;
-    return;
-#endif
+    constexpr bool kLowp = n == 8;   // 8 values per 16-byte pack: a 16-bit type
 #pragma unroll
     for (int e = 0; e < n; e += 2) {
-      const float d0 = 1.0f + ex2(-x[e] * 1.4426950408889634f);
-      const float d1 = 1.0f + ex2(-x[e + 1] * 1.4426950408889634f);
+      float d0, d1;
+      if (kLowp && NTB_SILU_FMA_EVERY &&
+          (e / 2) % (NTB_SILU_FMA_EVERY ? NTB_SILU_FMA_EVERY : 1) == NTB_SILU_FMA_EVERY - 1) {
+        const float2 t = ex2_fma(__fmul2_rn(make_float2(x[e], x[e + 1]),
+                                            make_float2(-1.4426950408889634f, -1.4426950408889634f)));
+        d0 = 1.0f + t.x;
+        d1 = 1.0f + t.y;
+      } else {
+        d0 = 1.0f + ex2(-x[e] * 1.4426950408889634f);
+        d1 = 1.0f + ex2(-x[e + 1] * 1.4426950408889634f);
+      }
       const float pr = d0 * d1;
       float s0, s1;
       if (pr < 0x1p126f) {

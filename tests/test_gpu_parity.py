@@ -383,6 +383,33 @@ def test_sdpa_peaky_scores_rescale(d):
     _close(got, oracle.sdpa(q, k, v), rtol=1e-2, atol=1e-2)
 
 
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("bhs", [(1, 80, 512), (2, 37, 700), (1, 1, 256), (1, 74, 256)])
+def test_sdpa_tail_split(d, bhs):
+    """Work-unit schedule (k_attn_sm100.cu launch_attn): full two-tile items
+    round-robin, then the last round's items as single-tile units on twice as
+    many CTAs (160 items on 148 SMs: 148 full + 24 single-tile units; 222
+    items: 148 + 148; 1 and 74 items: single-tile units only), with peaky
+    scores so the lazy O rescale runs inside single-tile units too.  Checked
+    against the oracle, and relaunches are bit-identical."""
+    b, h, s = bhs
+    rng = np.random.default_rng(s + h + d)
+    q = _r16((rng.standard_normal((b, h, s, d)) * 3).astype(np.float32), torch.float16)
+    k = _r16((rng.standard_normal((b, h, s, d)) * 3).astype(np.float32), torch.float16)
+    v = _r16(rng.uniform(-1, 1, (b, h, s, d)).astype(np.float32), torch.float16)
+    tq, tk, tv = (_t(x, torch.float16) for x in (q, k, v))
+    outs = []
+    for _ in range(2):
+        o = torch.zeros((b, h, s, d), device=DEV, dtype=torch.float16)
+        with _Paths() as pc:
+            backend.sdpa_launch(tq, tk, tv, o, 128, 128)
+            torch.cuda.synchronize()
+        assert pc.delta["attn_tc"] == 1
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1])
+    _close(outs[0], oracle.sdpa(q, k, v), rtol=1e-2, atol=1e-2)
+
+
 @pytest.mark.parametrize("dtype", DTS)
 @pytest.mark.parametrize("bshd", [(1, 256, 2, 64), (2, 300, 3, 128), (2, 1024, 4, 128),
                                   (3, 700, 40, 64), (1, 520, 64, 128)])
