@@ -12,6 +12,7 @@ import json
 import sys
 from collections import defaultdict
 
+L2_BYTES = 126 * 1024 * 1024
 rows = [r for r in csv.reader(io.StringIO(open(sys.argv[1]).read())) if r]
 hdr = next(r for r in rows if "ID" in r and "Metric Name" in r)
 ix = {h: i for i, h in enumerate(hdr)}
@@ -31,7 +32,7 @@ order = sys.argv[2].split(",")
 # the launches of each key are those between consecutive synchronisations;
 # kernels are attributed by name: every key's main kernel families
 FAMILY = {"softmax": "row_stream", "rms_norm": "row_stream", "add_2^20": "ew_vec",
-          "add_2^24": "ew_vec", "silu_2^24": "ew_vec", "mm": "gemm_pair", "addmm": "gemm_pair",
+          "add_2^24": "ew_stream", "silu_2^24": "ew_stream", "mm": "gemm_pair", "addmm": "gemm_pair",
           "bmm": "gemm_pair", "mm_f32": "gemm_tf32", "bmm_f32": "gemm_tf32",
           "conv2d": "conv_fused", "conv2d_f32": "gemm_tf32", "sdpa": "attn_fwd", "rope": "rope_vec",
           "sdpa_rope": "attn_fwd"}
@@ -45,13 +46,21 @@ for key in order:
     if k == len(ids):
         break
     d = data[ids[k]]
-    wr = max(d.get("dram__bytes_write.sum", 0), 32 * d.get("lts__t_sectors_srcunit_tex_op_write.sum", 0))
+    # bytes written = between the DRAM write counter and that plus one L2 of
+    # dirty lines still resident at kernel end; the SM-sourced L2 write
+    # sectors (32 B each) estimate it, capped by that bound (partial-sector
+    # stores count a sector per store)
+    dw = d.get("dram__bytes_write.sum", 0)
+    wr = max(dw, min(32 * d.get("lts__t_sectors_srcunit_tex_op_write.sum", 0), dw + L2_BYTES))
     out[key] = int(d.get("dram__bytes_read.sum", 0) + wr)
     k += 1
 out["_note"] = ("per launch, ncu on tools/traffic_probe.py (cold L2 per replay): "
-                "dram__bytes_read.sum + max(dram__bytes_write.sum, 32 B x lts__t_sectors_srcunit_tex_op_write.sum) "
-                "of the key's main kernel (writes left dirty in L2 at kernel end never reach DRAM "
-                "inside the capture; the L2 write sectors count them). sdpa_rope: the attention "
-                "kernel only (its K pre-pass is a separate rope_vec launch).")
+                "dram__bytes_read.sum + writes "
+                "of the key's main kernel, with writes = max(W, min(32 B x L2 write sectors, W + "
+                "126 MB)), W = dram__bytes_write.sum: writes left dirty in the L2 at kernel end "
+                "never reach DRAM inside the capture (the L2 write sectors count them), but at "
+                "most one L2 of them can (partial-sector stores, e.g. the attention epilogue's "
+                "16 B per row, count one sector per store). sdpa_rope: the attention kernel "
+                "only (its K pre-pass is a separate rope_vec launch).")
 json.dump(out, open("profiles/traffic.json", "w"), indent=1)
 print(json.dumps(out, indent=1))
