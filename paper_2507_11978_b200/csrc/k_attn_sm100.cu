@@ -75,8 +75,23 @@ __device__ long long g_attn_trace[2 * 64 * 8 + 64 * 8];
 #define TRACE_MMA(j, k)
 #endif
 
+#ifndef NTB_ATTN_ITRACE
+#define NTB_ATTN_ITRACE 0  // debug builds: item-boundary clock64 stamps of CTA 0 (first 16 units)
+#endif
+#if NTB_ATTN_ITRACE
+__device__ long long g_attn_items[3][16][4];
+#define ITR(g, it, k)                                                              \
+  if (blockIdx.x == 0 && lane == 0 && quad == 0 && (it) < 16) g_attn_items[g][it][k] = clock64();
+#define ITRM(it, k) \
+  if (blockIdx.x == 0 && (it) < 16) g_attn_items[2][it][k] = clock64();
+#else
+#define ITR(g, it, k)
+#define ITRM(it, k)
+#endif
+
 struct AttnMaps {
   CUtensorMap q, k, v;
+  CUtensorMap o;   // box {64, 32, 1, 1}, 128B swizzle (TMA-store epilogue), when o_tma
 };
 
 struct AttnParams {
@@ -86,6 +101,9 @@ struct AttnParams {
   // items as 2 * (n_items - n_full) = n_half SINGLE-TILE units, unit
   // n_full + u on CTA u: query tile u % 2 of item n_full + u / 2
   int n_full, n_half;
+  // epilogue: O rows staged in the unit's (then free) Q buffer and written by
+  // TMA stores (asynchronous to the softmax warps); else direct vector stores
+  int o_tma;
   float scale_log2;
   void* o;
   int64_t os[4];
@@ -169,7 +187,19 @@ __device__ __forceinline__ void rope_tile(uint8_t* tile, int chunk_bytes, int ro
 }
 
 #ifndef NTB_ATTN_QDB
-#define NTB_ATTN_QDB 0  // double-buffer Q in plain sdpa too (always with rope)
+#define NTB_ATTN_QDB 1  // double-buffer Q in plain sdpa too (always with rope)
+#endif
+#ifndef NTB_ATTN_STAGE_SMEM
+#define NTB_ATTN_STAGE_SMEM 0  // D = 128 plain sdpa: QB 1, 4-entry ring, dedicated epilogue staging
+#endif
+#ifndef NTB_ATTN_D64_QB2
+#define NTB_ATTN_D64_QB2 1  // D = 64: two Q buffers + cross-unit S issue too (82.7-83.9 vs 89.8-90.6 us with one)
+#endif
+#ifndef NTB_ATTN_NOSTORE
+#define NTB_ATTN_NOSTORE 0  // debug experiments only: skip the O stores (wrong output)
+#endif
+#ifndef NTB_ATTN_SEAM
+#define NTB_ATTN_SEAM 1  // with two Q buffers: next unit's first S MMAs issued inside this unit
 #endif
 
 template <int D, bool ROPE = false>
@@ -181,11 +211,23 @@ struct Layout {
   // Q buffers: with rope the next item's two query tiles are loaded and
   // rotated while the current item runs (the rotation is L2-latency bound,
   // ~5 us per item, and would otherwise stall the tensor core between items)
-  static constexpr int QB = (ROPE || NTB_ATTN_QDB) ? 2 : 1;
-  static constexpr int NS = D == 128 ? (QB == 2 ? 3 : 5) : 8;  // K/V ring entries
+  // Plain sdpa at D = 128 with STAGE_SMEM: one Q buffer, a 4-entry K/V ring
+  // and a dedicated 32 KB staging area for the TMA-store epilogue (one 4 KB
+  // box per softmax warp at a time); otherwise the epilogue stages in the
+  // unit's own (second) Q buffer.
+  static constexpr bool STAGE_SMEM = !ROPE && D == 128 && NTB_ATTN_STAGE_SMEM;
+  // measured per shape: D = 128 runs best with two Q
+  // buffers, the cross-unit S issue and the Q-buffer epilogue staging;
+  // D = 64 (8 KV tiles per unit at the paper's shape) with one Q buffer and
+  // the unit-by-unit order
+  static constexpr int QB = STAGE_SMEM ? 1 : ((ROPE || (NTB_ATTN_QDB && (D == 128 || NTB_ATTN_D64_QB2))) ? 2 : 1);
+  static constexpr bool SEAM = NTB_ATTN_SEAM && (D == 128 || ROPE || NTB_ATTN_D64_QB2);
+  static constexpr int NS = D == 128 ? (STAGE_SMEM ? 4 : (QB == 2 ? 3 : 5)) : 8;  // K/V ring entries
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = QB * 2 * Q_BYTES;
-  static constexpr int SMEM = OFF_KV + NS * SLOT + 1024;
+  static constexpr int OFF_STAGE = OFF_KV + NS * SLOT;
+  static constexpr int STAGE_BYTES = STAGE_SMEM ? 8 * 32 * 128 : 0;
+  static constexpr int SMEM = OFF_STAGE + STAGE_BYTES + 1024;
   static constexpr uint32_t T_S0 = 0, T_S1 = BN, T_O0 = 2 * BN, T_O1 = 2 * BN + D;
   static_assert(2 * BN + 2 * D <= 512, "TMEM budget");
   // D = 64 leaves 128 TMEM columns: each query tile gets its own P buffer
@@ -265,7 +307,9 @@ __global__ void __launch_bounds__(384, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < L::QB; ++i) {
       mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
+      // the MMA warp's commit after the unit's last S, plus (TMA-store
+      // epilogue) the 8 softmax warps once their staged O rows were read
+      mbar_init(&q_empty[i], (p.o_tma && !L::STAGE_SMEM) ? 9 : 1);
       mbar_init(&q_rot[i], 2);                  // rope warps 2-3
     }
     for (int i = 0; i < L::NS; ++i) {
@@ -323,9 +367,35 @@ __global__ void __launch_bounds__(384, 1)
         int item, half;
         unit_of(p, it, item, half);
         const int bh = item / p.n_qt, h = bh % p.H, b = bh / p.H;
-        if (L::QB == 1) load_q(it);
-        else if (it + 1 < nu) load_q(it + 1);
+        // one Q buffer: this unit's Q after its first K/V tile (the buffer frees
+        // only when the previous unit's last S completed; K_0, V_0 need not
+        // wait).  Two: the next unit's Q after this unit's last K/V tile (its
+        // buffer frees when unit it-1's epilogue staging has been read).
+        if (L::QB == 1 && (it == 0 || !L::SEAM)) load_q(it);
+        // rope: the next unit's Q now, so its rotation (L2-latency bound,
+        // ~5 us) is done long before the unit starts (the rope epilogue
+        // stores O directly, so the buffer is free after the unit's last S)
+        if (L::QB == 2 && ROPE && it + 1 < nu) load_q(it + 1);
+
         for (int j = 0; j < n_kv; ++j) {
+#if !NTB_ATTN_NO_QPREFETCH
+          // the next unit's query rows into L2 a few tiles before its TMA
+          // load, which is issued only when this unit's last S MMA frees the
+          // Q buffer (earlier, the K/V stream of 148 CTAs evicts them again)
+          if (L::SEAM && j == (n_kv > 4 ? n_kv - 4 : 0) && it + 1 < nu) {
+            int nitem, nhalf;
+            unit_of(p, it + 1, nitem, nhalf);
+            const int nqt = nitem % p.n_qt, nbh = nitem / p.n_qt;
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+              if (nhalf >= 0 && g == 1) break;
+              const int tile = nhalf < 0 ? g : nhalf;
+#pragma unroll
+              for (int ch = 0; ch < L::DCH; ++ch)
+                tma_prefetch_4d(&maps.q, ch * 64, nqt * 2 * BM + tile * BM, nbh % p.H, nbh / p.H);
+            }
+          }
+#endif
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv, ++c) {
             const uint32_t slot = c % L::NS;
@@ -337,6 +407,8 @@ __global__ void __launch_bounds__(384, 1)
               tma_load_4d(dst + ch * L::CH, kv ? &maps.v : &maps.k, &kv_full[slot], ch * 64, j * BN,
                           h, b);
           }
+          if (L::QB == 1 && L::SEAM && it > 0 && j == 0) load_q(it);
+          if (L::QB == 2 && !ROPE && j == n_kv - 1 && it + 1 < nu) load_q(it + 1);
         }
       }
     }
@@ -379,38 +451,70 @@ __global__ void __launch_bounds__(384, 1)
         }
       };
       const int nu = n_units(p);
+      auto unit_two = [&](int u) {
+        int i, h;
+        unit_of(p, u, i, h);
+        return h < 0;
+      };
+      auto wait_q = [&](int u) {
+        const int b = u % L::QB;
+        mbar_wait(ROPE ? &q_rot[b] : &q_full[b], (u / L::QB) & 1);
+        tc_fence_after();
+      };
+      // S_g of KV tile jn of unit un (K at ring sequence kseq), then the
+      // releases that follow the LAST S reading those buffers: K_jn after
+      // S1 (S0 for a single-tile unit), the unit's Q after its last tile's S
+      auto s_and_release = [&](int g, int un, int jn, bool two_un, uint32_t kseq) {
+        qb = un % L::QB;
+        issue_s(g, kseq);
+        if (g == (two_un ? 1 : 0)) {
+          mma_commit(&kv_empty[kseq % L::NS]);
+          if (jn == n_kv - 1) mma_commit(&q_empty[qb]);
+        }
+      };
+      // SEAM: the next unit's first S MMAs are issued right behind this unit's
+      // last P.V of the same query tile, so the ping-pong runs on across unit
+      // boundaries instead of restarting after both warpgroups' epilogues
+      // (with one Q buffer, the next unit's Q is loaded - from L2, prefetched
+      // a few tiles earlier - once this unit's last S has read the buffer).
+      constexpr bool SEAM = L::SEAM;
       for (it = 0; it < nu; ++it) {
-        int item, half;
-        unit_of(p, it, item, half);
-        (void)item;
         // two: the ping-pong of both query tiles; otherwise tile 0 alone, and
         // the K / V / Q buffers are released after its own MMAs
-        const bool two = half < 0;
-        qb = it % L::QB;
-        mbar_wait(ROPE ? &q_rot[qb] : &q_full[qb], (it / L::QB) & 1);
-        tc_fence_after();
-        wait_kv(c);
-        issue_s(0, c);
-        if (two) issue_s(1, c);
-        mma_commit(&kv_empty[c % L::NS]);
-        if (n_kv == 1) mma_commit(&q_empty[qb]);
+        const bool two = unit_two(it);
+        if (!SEAM || it == 0) {
+          ITRM(it, 0)
+          wait_q(it);
+          ITRM(it, 1)
+          wait_kv(c);
+          ITRM(it, 2)
+          s_and_release(0, it, 0, two, c);
+          if (two) s_and_release(1, it, 0, two, c);
+          ITRM(it, 3)
+        }
         for (int j = 0; j < n_kv; ++j, ++t) {
           const bool more = j + 1 < n_kv;
+          const bool nxt = SEAM && !more && it + 1 < nu;   // next S belongs to unit it + 1
+          const bool hs = more || nxt;                      // a next S exists
+          const int un = more ? it : it + 1, jn = more ? j + 1 : 0;
+          const bool two_n = more ? two : (nxt ? unit_two(it + 1) : false);
           const uint32_t kseq = c + 2 * j, vseq = kseq + 1, knext = kseq + 2;
-          auto next_s0 = [&]() {
-            issue_s(0, knext);
-            if (!two) {
-              mma_commit(&kv_empty[knext % L::NS]);
-              if (j + 2 == n_kv) mma_commit(&q_empty[qb]);
+          auto next_s = [&](int g) {
+            if (nxt && g == 0) {
+              ITRM(it + 1, 1)
+              wait_q(it + 1);
+              ITRM(it + 1, 2)
             }
+            if (g == 0 || two_n) s_and_release(g, un, jn, two_n, knext);
+            if (nxt && g == 0) { ITRM(it + 1, 3) }
           };
           // ---- query tile 0
           TRACE_MMA(j, 0)
-          if (L::SEP_P && more) {
+          if (L::SEP_P && hs && !nxt) {
             // S_0 columns already read by the softmax: next S right away
             mbar_wait(&s_free[0], t & 1);
             wait_kv(knext);
-            next_s0();
+            next_s(0);
           }
           mbar_wait(&p_full[0][0], t & 1);
           tc_fence_after();
@@ -430,23 +534,23 @@ __global__ void __launch_bounds__(384, 1)
           TRACE_MMA(j, 2)
           if (!two) mma_commit(&kv_empty[vseq % L::NS]);
           if (L::SEP_P) mma_commit(&pv_done[0]);
-          if (more) {
-            if (!L::SEP_P) {
-              wait_kv(knext);
-              TRACE_MMA(j, 3)
-              next_s0();
-            }
-          } else {
-            mma_commit(&o_full[0]);
+          if (!more) mma_commit(&o_full[0]);   // before any next-unit S: O0 is final
+          if (L::SEP_P && nxt) {
+            mbar_wait(&s_free[0], t & 1);
+            wait_kv(knext);
+            next_s(0);
+          }
+          if (hs && !L::SEP_P) {
+            wait_kv(knext);
+            TRACE_MMA(j, 3)
+            next_s(0);
           }
           if (!two) continue;
           // ---- query tile 1
           TRACE_MMA(j, 4)
-          if (L::SEP_P && more) {
+          if (L::SEP_P && hs && two_n && !nxt) {
             mbar_wait(&s_free[1], t & 1);
-            issue_s(1, knext);
-            mma_commit(&kv_empty[knext % L::NS]);
-            if (j + 2 == n_kv) mma_commit(&q_empty[qb]);
+            next_s(1);
           }
           mbar_wait(&p_full[1][0], t & 1);
           tc_fence_after();
@@ -464,15 +568,18 @@ __global__ void __launch_bounds__(384, 1)
           }
           mma_commit(&kv_empty[vseq % L::NS]);
           if (L::SEP_P) mma_commit(&pv_done[1]);
-          if (more) {
-            if (!L::SEP_P) {
-              issue_s(1, knext);
-              mma_commit(&kv_empty[knext % L::NS]);
-              if (j + 2 == n_kv) mma_commit(&q_empty[qb]);
-            }
-          } else {
-            mma_commit(&o_full[1]);
+          if (!more) mma_commit(&o_full[1]);
+          if (L::SEP_P && nxt && two_n) {
+            mbar_wait(&s_free[1], t & 1);
+            next_s(1);
           }
+          if (hs && two_n && !L::SEP_P) next_s(1);
+#if NTB_ATTN_ITRACE
+          if (nxt) {   // debug: when did the next unit's S0 complete?
+            mbar_wait(&s_full[0], (t + 1) & 1);
+            ITRM(it + 1, 0)
+          }
+#endif
           TRACE_MMA(j, 6)
         }
         c += 2 * n_kv;
@@ -512,6 +619,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t t_o = tmem + (g ? L::T_O1 : L::T_O0) + lane_off;
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     uint32_t t = 0;
+    int stage_pending = -1;   // Q buffer holding this warp's staged O rows of the last unit
     const int nu = n_units(p);
     for (int it = 0; it < nu; ++it) {
       int item, half;
@@ -526,6 +634,7 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&s_full[g], t & 1);
         tc_fence_after();
         TRACE_SM(g, j, 1)
+        if (j == 0) { ITR(g, it, 0) }
         const int kvalid = p.Sk - j * BN;
         uint32_t v[BN];
 #pragma unroll
@@ -629,11 +738,22 @@ __global__ void __launch_bounds__(384, 1)
         }
         l = fmaf(l, alpha, (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
         m_used = m_new;
+        if (stage_pending >= 0 && (j >= 1 || j == n_kv - 1)) {
+          // the previous unit's staged O rows: long read by the TMA by now;
+          // release that Q buffer to the producer
+          if (lane == 0) {
+            bulk_wait_read<0>();
+            mbar_arrive(&q_empty[stage_pending]);
+          }
+          stage_pending = -1;
+        }
         TRACE_SM(g, j, 5)
       }
       // epilogue: O row -> registers, release O, then O / l -> global
+      ITR(g, it, 1)
       mbar_wait(&o_full[g], it & 1);
       tc_fence_after();
+      ITR(g, it, 2)
       uint32_t o[D];
 #pragma unroll
       for (int ch = 0; ch < D / 32; ++ch) tmem_ld_32x32b_x32(t_o + ch * 32, o + ch * 32);
@@ -643,10 +763,82 @@ __global__ void __launch_bounds__(384, 1)
       if (lane == 0) mbar_arrive(&o_empty[g]);
       const float inv = 1.f / l;
       const int qrow = qt * 2 * BM + tile * BM + row;
-      if (qrow < p.Sq) {
+      if (p.o_tma) {
+        // stage this warp's 32 rows x D columns, 64 columns (128 B) per
+        // 4 KB box, 128B-swizzled (row r's 16-byte chunk q at q ^ (r & 7):
+        // conflict-free), in the unit's Q buffer - free once the unit's last
+        // S MMA completed (o_full implies it) - and let the TMA store them
+        // (rows past S_q clipped); the producer reloads the buffer only
+        // after every warp's TMA has read its staging (q_empty)
+        const int qbuf = it % L::QB;
+        uint8_t* stage = L::STAGE_SMEM
+                             ? smem + L::OFF_STAGE + (g * 4 + quad) * (32 * 128)
+                             : smem + L::OFF_Q + qbuf * 2 * L::Q_BYTES +
+                                   ((g * 4 + quad) * L::DCH) * (32 * 128);
+        const int row0 = qt * 2 * BM + tile * BM + quad * 32;
+#pragma unroll
+        for (int ch = 0; ch < L::DCH; ++ch) {
+          uint8_t* box = L::STAGE_SMEM ? stage : stage + ch * (32 * 128);
+          if (L::STAGE_SMEM) {
+            // one 4 KB box per warp: the previous box (of this or the last
+            // unit) must have been read by its TMA store
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+          }
+          const uint32_t base = smem_u32(box) + lane * 128;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              w[e] = pack2<BF16>(__uint_as_float(o[ch * 64 + q * 8 + e * 2]) * inv,
+                                 __uint_as_float(o[ch * 64 + q * 8 + e * 2 + 1]) * inv);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + ((q ^ (lane & 7)) << 4)),
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                         : "memory");
+          }
+          if (L::STAGE_SMEM) {
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(&maps.o, box, ch * 64, row0, h, b);
+              bulk_commit();
+            }
+          }
+        }
+        if (!L::STAGE_SMEM) {
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int ch = 0; ch < L::DCH; ++ch)
+              tma_store_4d(&maps.o, stage + ch * (32 * 128), ch * 64, row0, h, b);
+            bulk_commit();
+          }
+          stage_pending = qbuf;   // q_empty arrive once the TMA has read it (below)
+        }
+        ITR(g, it, 3)
+      } else if (qrow < p.Sq && !NTB_ATTN_NOSTORE) {
         char* obase = reinterpret_cast<char*>(p.o) +
                       ((int64_t)b * p.os[0] + (int64_t)h * p.os[1] + (int64_t)qrow * p.os[2]) * 2;
-        if (p.os[3] == 1 && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0)) {
+        if (D == 128 && p.os[3] == 1 && ((reinterpret_cast<uintptr_t>(obase) & 31) == 0)) {
+          // 256-bit stores: every lane writes whole 32-byte sectors of its row
+          // (with 128-bit stores each warp store half-filled 32 sectors, and
+          // the warp's next barrier wait queued behind their drain)
+#pragma unroll
+          for (int u = 0; u < D / 16; ++u) {
+            uint32_t q8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              q8[e] = pack2<BF16>(__uint_as_float(o[u * 16 + e * 2]) * inv,
+                                  __uint_as_float(o[u * 16 + e * 2 + 1]) * inv);
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(obase + u * 32),
+                         "r"(q8[0]), "r"(q8[1]), "r"(q8[2]), "r"(q8[3]), "r"(q8[4]), "r"(q8[5]),
+                         "r"(q8[6]), "r"(q8[7])
+                         : "memory");
+          }
+          ITR(g, it, 3)
+        } else if (p.os[3] == 1 && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0)) {
           uint4* dst = reinterpret_cast<uint4*>(obase);
 #pragma unroll
           for (int u = 0; u < D / 8; ++u) {
@@ -657,6 +849,7 @@ __global__ void __launch_bounds__(384, 1)
                                   __uint_as_float(o[u * 8 + e * 2 + 1]) * inv);
             dst[u] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
           }
+          ITR(g, it, 3)
         } else {
 #pragma unroll
           for (int i = 0; i < D; ++i) {
@@ -671,6 +864,7 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   }
+  if (p.o_tma && warp >= 4 && lane == 0) bulk_wait<0>();   // O stores complete before exit
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
@@ -685,6 +879,9 @@ int launch_attn(const AttnMaps& maps, AttnParams p, cudaStream_t s) {
   static size_t attr[kMaxDevices] = {};
   cudaError_t e = smem_attr_once(k, L::SMEM, attr);
   if (e != cudaSuccess) return cuda_fail(e, "attention smem attribute");
+  // the TMA-store epilogue stages in a second Q buffer or its own area
+  // (not with rope: its next Q is loaded and rotated a whole unit ahead)
+  if ((L::QB != 2 && !L::STAGE_SMEM) || ROPE) p.o_tma = 0;
   // Tail split: when the last round of items would leave more than half of
   // the CTAs idle, its items run as two single-tile units each on twice as
   // many CTAs (a single-tile unit takes ~half to ~3/4 of an item: the chain
@@ -729,6 +926,23 @@ int launch_attn(const AttnMaps& maps, AttnParams p, cudaStream_t s) {
     }
   }
 #endif
+#if NTB_ATTN_ITRACE
+  {
+    static long long h[3][16][4];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, g_attn_items, sizeof(h));
+    const long long t0 = h[0][0][0];
+    for (int it = 0; it < 16; ++it)
+      for (int g = 0; g < 2; ++g)
+        fprintf(stderr, "unit %2d g%d: S0 ready @%9lld  tiles %7lld  o_full wait %6lld  epilogue %6lld  next S0 after %6lld\n",
+                it, g, h[g][it][0] - t0, h[g][it][1] - h[g][it][0], h[g][it][2] - h[g][it][1],
+                h[g][it][3] - h[g][it][2], it < 15 ? h[g][it + 1][0] - h[g][it][3] : 0);
+    for (int it = 0; it < 16; ++it)
+      fprintf(stderr, "unit %2d mma: S0 done @%9lld  (S0 waits started %6lld before) q wait %6lld  S0 issue %6lld\n", it,
+              h[2][it][0] - t0, h[2][it][1] - h[2][it][0], h[2][it][2] - h[2][it][1],
+              h[2][it][3] - h[2][it][2]);
+  }
+#endif
   return check_launch("sdpa tcgen05", NTB_PATH_ATTN_TC);
 }
 
@@ -740,6 +954,17 @@ bool map4(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int64_t D, i
   uint64_t dims[4] = {(uint64_t)D, (uint64_t)S, (uint64_t)H, (uint64_t)B};
   uint64_t str[3] = {(uint64_t)st[2] * 2, (uint64_t)st[1] * 2, (uint64_t)st[0] * 2};
   uint32_t box[4] = {64, rows, 1, 1};
+  return encode_tmap(m, dt, 4, base, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+bool map4o(CUtensorMap* m, CUtensorMapDataType dt, void* base, int64_t D, int64_t S, int64_t H,
+           int64_t B, const int64_t* st) {
+  if (st[3] != 1) return false;
+  for (int i = 0; i < 3; ++i)
+    if ((st[i] * 2) % 16 || st[i] <= 0) return false;
+  uint64_t dims[4] = {(uint64_t)D, (uint64_t)S, (uint64_t)H, (uint64_t)B};
+  uint64_t str[3] = {(uint64_t)st[2] * 2, (uint64_t)st[1] * 2, (uint64_t)st[0] * 2};
+  uint32_t box[4] = {64, 32, 1, 1};
   return encode_tmap(m, dt, 4, base, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
@@ -774,6 +999,14 @@ int attn_sm100(const AttnDesc& a, int dtype, cudaStream_t s, const RopeTables* r
       !map4(&maps.v, dt, a.v, a.D, a.Sk, a.H, a.B, vs, BN))
     return NTB_ERR_UNSUPPORTED;
   AttnParams p;
+  // O through TMA stores when its layout allows a tensor map (unit inner
+  // stride, 16-byte aligned base and strides)
+  {
+    int64_t os[4] = {a.os[0], a.os[1], a.os[2], a.os[3]};
+    fix(os, a.B, a.H, a.Sq, a.D);
+    static const bool direct = getenv("NTB_ATTN_DIRECT_STORE") != nullptr;
+    p.o_tma = !direct && aligned16(a.o) && map4o(&maps.o, dt, a.o, a.D, a.Sq, a.H, a.B, os);
+  }
   p.B = (int)a.B;
   p.H = (int)a.H;
   p.Sq = (int)a.Sq;
