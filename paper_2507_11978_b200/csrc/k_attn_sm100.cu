@@ -222,6 +222,13 @@ struct Layout {
   // the unit-by-unit order
   static constexpr int QB = STAGE_SMEM ? 1 : ((ROPE || (NTB_ATTN_QDB && (D == 128 || NTB_ATTN_D64_QB2))) ? 2 : 1);
   static constexpr bool SEAM = NTB_ATTN_SEAM && (D == 128 || ROPE || NTB_ATTN_D64_QB2);
+  // (two Q buffers) EARLY_Q: the next unit's Q is requested right after this
+  // unit's first K/V tile and each warp releases its staged O rows as soon
+  // as the TMA has read them (D = 64, rope: 82 vs 87 us at the paper shape);
+  // otherwise the next Q is requested after the unit's last K/V tile and the
+  // staging is released during the next unit's second tile (D = 128: 6.92-
+  // 6.95 vs 7.05-7.33 ms)
+  static constexpr bool EARLY_Q = D == 64 || ROPE;
   static constexpr int NS = D == 128 ? (STAGE_SMEM ? 4 : (QB == 2 ? 3 : 5)) : 8;  // K/V ring entries
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = QB * 2 * Q_BYTES;
@@ -372,10 +379,7 @@ __global__ void __launch_bounds__(384, 1)
         // wait).  Two: the next unit's Q after this unit's last K/V tile (its
         // buffer frees when unit it-1's epilogue staging has been read).
         if (L::QB == 1 && (it == 0 || !L::SEAM)) load_q(it);
-        // rope: the next unit's Q now, so its rotation (L2-latency bound,
-        // ~5 us) is done long before the unit starts (the rope epilogue
-        // stores O directly, so the buffer is free after the unit's last S)
-        if (L::QB == 2 && ROPE && it + 1 < nu) load_q(it + 1);
+
 
         for (int j = 0; j < n_kv; ++j) {
 #if !NTB_ATTN_NO_QPREFETCH
@@ -408,7 +412,11 @@ __global__ void __launch_bounds__(384, 1)
                           h, b);
           }
           if (L::QB == 1 && L::SEAM && it > 0 && j == 0) load_q(it);
-          if (L::QB == 2 && !ROPE && j == n_kv - 1 && it + 1 < nu) load_q(it + 1);
+          // two Q buffers: the next unit's Q after this unit's first (EARLY_Q)
+          // or last K/V tile (its buffer frees when unit it-1's last S
+          // completed and its epilogue's staged O rows were read; with rope
+          // it is then rotated - ~5 us, L2-latency bound - well before use)
+          if (L::QB == 2 && j == (L::EARLY_Q ? 0 : n_kv - 1) && it + 1 < nu) load_q(it + 1);
         }
       }
     }
@@ -619,7 +627,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t t_o = tmem + (g ? L::T_O1 : L::T_O0) + lane_off;
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     uint32_t t = 0;
-    int stage_pending = -1;   // Q buffer holding this warp's staged O rows of the last unit
+    int stage_pending = -1;   // !EARLY_Q: Q buffer holding this warp's staged O rows
     const int nu = n_units(p);
     for (int it = 0; it < nu; ++it) {
       int item, half;
@@ -738,7 +746,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         l = fmaf(l, alpha, (sum2[0].x + sum2[0].y) + (sum2[1].x + sum2[1].y));
         m_used = m_new;
-        if (stage_pending >= 0 && (j >= 1 || j == n_kv - 1)) {
+        if (!L::EARLY_Q && stage_pending >= 0 && (j >= 1 || j == n_kv - 1)) {
           // the previous unit's staged O rows: long read by the TMA by now;
           // release that Q buffer to the producer
           if (lane == 0) {
@@ -747,6 +755,7 @@ __global__ void __launch_bounds__(384, 1)
           }
           stage_pending = -1;
         }
+
         TRACE_SM(g, j, 5)
       }
       // epilogue: O row -> registers, release O, then O / l -> global
@@ -814,8 +823,14 @@ __global__ void __launch_bounds__(384, 1)
             for (int ch = 0; ch < L::DCH; ++ch)
               tma_store_4d(&maps.o, stage + ch * (32 * 128), ch * 64, row0, h, b);
             bulk_commit();
+            if (L::EARLY_Q) {
+              // the Q buffer goes back to the producer once the TMA has read
+              // the staged rows (a few hundred cycles)
+              bulk_wait_read<0>();
+              mbar_arrive(&q_empty[qbuf]);
+            }
           }
-          stage_pending = qbuf;   // q_empty arrive once the TMA has read it (below)
+          if (!L::EARLY_Q) stage_pending = qbuf;   // released during the next unit (below)
         }
         ITR(g, it, 3)
       } else if (qrow < p.Sq && !NTB_ATTN_NOSTORE) {
@@ -880,8 +895,7 @@ int launch_attn(const AttnMaps& maps, AttnParams p, cudaStream_t s) {
   cudaError_t e = smem_attr_once(k, L::SMEM, attr);
   if (e != cudaSuccess) return cuda_fail(e, "attention smem attribute");
   // the TMA-store epilogue stages in a second Q buffer or its own area
-  // (not with rope: its next Q is loaded and rotated a whole unit ahead)
-  if ((L::QB != 2 && !L::STAGE_SMEM) || ROPE) p.o_tma = 0;
+  if (L::QB != 2 && !L::STAGE_SMEM) p.o_tma = 0;
   // Tail split: when the last round of items would leave more than half of
   // the CTAs idle, its items run as two single-tile units each on twice as
   // many CTAs (a single-tile unit takes ~half to ~3/4 of an item: the chain
