@@ -573,6 +573,36 @@ def test_sdpa_strided_views():
     _close(got, ref, rtol=1e-2, atol=1e-2)
 
 
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("olayout", ["bshd", "offset16", "inner2"])
+def test_sdpa_output_layouts(d, olayout):
+    """The epilogue's store paths: O through TMA stores staged in shared
+    memory (any 16-byte-aligned unit-inner-stride layout: (B, S, H, D)
+    storage viewed as (B, H, S, D); a base 16 but not 32 bytes aligned) and
+    the direct-store fallback (inner stride 2), with S_q not a multiple of
+    the 32-row store box; multi-unit schedules (148+ units)."""
+    rng = np.random.default_rng(d)
+    b, h, s = 2, 80, 333
+    q, k, v = (_r16(rng.uniform(-1, 1, (b, h, s, d)).astype(np.float32), torch.float16)
+               for _ in range(3))
+    if olayout == "bshd":
+        store = torch.zeros((b, s, h, d), device=DEV, dtype=torch.float16)
+        o = store.transpose(1, 2)
+    elif olayout == "offset16":
+        store = torch.zeros(b * h * s * d + 8, device=DEV, dtype=torch.float16)
+        o = store[8:].view(b, h, s, d)
+    else:
+        store = torch.zeros((b, h, s, 2 * d), device=DEV, dtype=torch.float16)
+        o = store[..., ::2]
+    with _Paths() as pc:
+        backend.sdpa_launch(*(_t(x, torch.float16) for x in (q, k, v)), o, 128, 128)
+        torch.cuda.synchronize()
+    assert pc.delta["attn_tc"] == 1
+    _close(o, oracle.sdpa(q, k, v), rtol=1e-2, atol=1e-2)
+    if olayout == "inner2":   # the interleaved columns were not touched
+        assert torch.count_nonzero(store[..., 1::2]).item() == 0
+
+
 @pytest.mark.parametrize("dtype", DTS + [torch.float32])
 @pytest.mark.parametrize("shape", [(1, 4, 2, 16), (2, 64, 8, 128), (2, 128, 32, 64)])
 def test_rope(dtype, shape):
