@@ -195,9 +195,6 @@ __device__ __forceinline__ void rope_tile(uint8_t* tile, int chunk_bytes, int ro
 #ifndef NTB_ATTN_D64_QB2
 #define NTB_ATTN_D64_QB2 1  // D = 64: two Q buffers + cross-unit S issue too (82.7-83.9 vs 89.8-90.6 us with one)
 #endif
-#ifndef NTB_ATTN_NOSTORE
-#define NTB_ATTN_NOSTORE 0  // debug experiments only: skip the O stores (wrong output)
-#endif
 #ifndef NTB_ATTN_SEAM
 #define NTB_ATTN_SEAM 1  // with two Q buffers: next unit's first S MMAs issued inside this unit
 #endif
@@ -582,12 +579,6 @@ __global__ void __launch_bounds__(384, 1)
             next_s(1);
           }
           if (hs && two_n && !L::SEP_P) next_s(1);
-#if NTB_ATTN_ITRACE
-          if (nxt) {   // debug: when did the next unit's S0 complete?
-            mbar_wait(&s_full[0], (t + 1) & 1);
-            ITRM(it + 1, 0)
-          }
-#endif
           TRACE_MMA(j, 6)
         }
         c += 2 * n_kv;
@@ -833,7 +824,7 @@ __global__ void __launch_bounds__(384, 1)
           if (!L::EARLY_Q) stage_pending = qbuf;   // released during the next unit (below)
         }
         ITR(g, it, 3)
-      } else if (qrow < p.Sq && !NTB_ATTN_NOSTORE) {
+      } else if (qrow < p.Sq) {
         char* obase = reinterpret_cast<char*>(p.o) +
                       ((int64_t)b * p.os[0] + (int64_t)h * p.os[1] + (int64_t)qrow * p.os[2]) * 2;
         if (D == 128 && p.os[3] == 1 && ((reinterpret_cast<uintptr_t>(obase) & 31) == 0)) {
@@ -952,7 +943,7 @@ int launch_attn(const AttnMaps& maps, AttnParams p, cudaStream_t s) {
                 it, g, h[g][it][0] - t0, h[g][it][1] - h[g][it][0], h[g][it][2] - h[g][it][1],
                 h[g][it][3] - h[g][it][2], it < 15 ? h[g][it + 1][0] - h[g][it][3] : 0);
     for (int it = 0; it < 16; ++it)
-      fprintf(stderr, "unit %2d mma: S0 done @%9lld  (S0 waits started %6lld before) q wait %6lld  S0 issue %6lld\n", it,
+      fprintf(stderr, "unit %2d mma: start @%9lld  q wait %6lld  K0 wait %6lld  S issue %6lld\n", it,
               h[2][it][0] - t0, h[2][it][1] - h[2][it][0], h[2][it][2] - h[2][it][1],
               h[2][it][3] - h[2][it][2]);
   }
