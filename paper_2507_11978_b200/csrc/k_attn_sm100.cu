@@ -113,6 +113,15 @@ struct AttnParams {
   int64_t sq_rs, cq_rs;
 };
 
+// a * b + c with 16-bit a, b and an fp32 accumulate (FHFMA)
+template <bool BF16>
+__device__ __forceinline__ float hfma(uint16_t a, uint16_t b, float c) {
+  float d;
+  if constexpr (BF16) asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  else asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  return d;
+}
+
 // Rotate `rows` rows of a 128B-swizzled K-major tile in place (half-split
 // rotary embedding, x0 = columns [0, D/2), x1 = [D/2, D)):
 //   x0' = x0*c - x1*s,  x1' = x0*s + x1*c   (fp32, rounded to 16 bit)
@@ -162,23 +171,21 @@ __device__ __forceinline__ void rope_tile(uint8_t* tile, int chunk_bytes, int ro
       uint32_t o0[4], o1[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        float2 fa, fb, fc, fs;
-        if constexpr (BF16) {
-          fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a[e]));
-          fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b[e]));
-          fc = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&cc[e]));
-          fs = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ss[e]));
-        } else {
-          fa = __half22float2(*reinterpret_cast<const __half2*>(&a[e]));
-          fb = __half22float2(*reinterpret_cast<const __half2*>(&b[e]));
-          fc = __half22float2(*reinterpret_cast<const __half2*>(&cc[e]));
-          fs = __half22float2(*reinterpret_cast<const __half2*>(&ss[e]));
+        // x0' = x0 c - x1 s, x1' = x0 s + x1 c with mixed-precision FMAs
+        // (16-bit operands, fp32 accumulate: the 16 x 16-bit products are
+        // exact in fp32, so this is bit-identical to converting first and
+        // computing in fp32 as the standalone rope kernel does, with no
+        // conversion instructions)
+        float r0[2], r1[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint16_t x0 = (uint16_t)(a[e] >> (16 * hh)), x1 = (uint16_t)(b[e] >> (16 * hh));
+          const uint16_t c = (uint16_t)(cc[e] >> (16 * hh)), sn = (uint16_t)(ss[e] >> (16 * hh));
+          r0[hh] = hfma<BF16>(x0, c, -hfma<BF16>(x1, sn, 0.f));
+          r1[hh] = hfma<BF16>(x1, c, hfma<BF16>(x0, sn, 0.f));
         }
-        // same expression as the standalone rope kernel (k_rope.cu)
-        const float r0x = fa.x * fc.x - fb.x * fs.x, r0y = fa.y * fc.y - fb.y * fs.y;
-        const float r1x = fa.x * fs.x + fb.x * fc.x, r1y = fa.y * fs.y + fb.y * fc.y;
-        o0[e] = BF16 ? sm100::pack_bf16(r0x, r0y) : sm100::pack_f16(r0x, r0y);
-        o1[e] = BF16 ? sm100::pack_bf16(r1x, r1y) : sm100::pack_f16(r1x, r1y);
+        o0[e] = BF16 ? sm100::pack_bf16(r0[0], r0[1]) : sm100::pack_f16(r0[0], r0[1]);
+        o1[e] = BF16 ? sm100::pack_bf16(r1[0], r1[1]) : sm100::pack_f16(r1[0], r1[1]);
       }
       *p0[k] = make_uint4(o0[0], o0[1], o0[2], o0[3]);
       *p1[k] = make_uint4(o1[0], o1[1], o1[2], o1[3]);
