@@ -420,7 +420,13 @@ __global__ void __launch_bounds__(384, 1)
           // or last K/V tile (its buffer frees when unit it-1's last S
           // completed and its epilogue's staged O rows were read; with rope
           // it is then rotated - ~5 us, L2-latency bound - well before use)
-          if (L::QB == 2 && j == (L::EARLY_Q ? 0 : n_kv - 1) && it + 1 < nu) load_q(it + 1);
+          // (EARLY_Q: a few tiles into the unit rather than at its first
+          // tile - the producer runs ~NS/2 tiles ahead of the MMAs, and the
+          // buffer is released by the previous unit's epilogue, so waiting
+          // for it at tile 0 would stall this unit's next K/V loads)
+          if (L::QB == 2 && j == (L::EARLY_Q ? (n_kv > L::NS / 2 ? L::NS / 2 : n_kv - 1) : n_kv - 1) &&
+              it + 1 < nu)
+            load_q(it + 1);
         }
       }
     }
