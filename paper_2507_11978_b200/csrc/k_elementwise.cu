@@ -328,9 +328,10 @@ static int run_ew(const LaunchArgs& A) {
     if (stream && try_ew_stream<T, Op>(a, b, out, n_vec, A.stream))
       return check_launch("elementwise stream", NTB_PATH_EW_STREAM);
     // one wave of 8 resident 256-thread CTAs per SM, each thread U vectors
-    // per input in flight per iteration (measured: 8 for fp32 add 2^24 =
-    // 0.97 of HBM, 4 for the 16-bit silu 2^24 = 0.80)
-    constexpr int U = NTB_EW_UNROLL ? NTB_EW_UNROLL : (sizeof(T) == 4 ? 8 : 4);
+    // per input in flight per iteration; this kernel now serves launches
+    // below 32 MB, where 4 is best (add fp32 2^20: 2.88-3.08 us vs 3.06-3.13
+    // with 8, 3.51-3.66 with 2, 3.93-4.07 with 16)
+    constexpr int U = NTB_EW_UNROLL ? NTB_EW_UNROLL : 4;
     int64_t blocks = cdiv64(n_vec, 256 * U);
     int64_t cap = (int64_t)sms * 8;
     if (blocks > cap) blocks = cap;
