@@ -196,9 +196,6 @@ __device__ __forceinline__ void rope_tile(uint8_t* tile, int chunk_bytes, int ro
 #ifndef NTB_ATTN_QDB
 #define NTB_ATTN_QDB 1  // double-buffer Q in plain sdpa too (always with rope)
 #endif
-#ifndef NTB_ATTN_STAGE_SMEM
-#define NTB_ATTN_STAGE_SMEM 0  // D = 128 plain sdpa: QB 1, 4-entry ring, dedicated epilogue staging
-#endif
 #ifndef NTB_ATTN_D64_QB2
 #define NTB_ATTN_D64_QB2 1  // D = 64: two Q buffers + cross-unit S issue too (82.7-83.9 vs 89.8-90.6 us with one)
 #endif
@@ -215,16 +212,11 @@ struct Layout {
   // Q buffers: with rope the next item's two query tiles are loaded and
   // rotated while the current item runs (the rotation is L2-latency bound,
   // ~5 us per item, and would otherwise stall the tensor core between items)
-  // Plain sdpa at D = 128 with STAGE_SMEM: one Q buffer, a 4-entry K/V ring
-  // and a dedicated 32 KB staging area for the TMA-store epilogue (one 4 KB
-  // box per softmax warp at a time); otherwise the epilogue stages in the
-  // unit's own (second) Q buffer.
-  static constexpr bool STAGE_SMEM = !ROPE && D == 128 && NTB_ATTN_STAGE_SMEM;
   // measured per shape: D = 128 runs best with two Q
   // buffers, the cross-unit S issue and the Q-buffer epilogue staging;
   // D = 64 (8 KV tiles per unit at the paper's shape) with one Q buffer and
   // the unit-by-unit order
-  static constexpr int QB = STAGE_SMEM ? 1 : ((ROPE || (NTB_ATTN_QDB && (D == 128 || NTB_ATTN_D64_QB2))) ? 2 : 1);
+  static constexpr int QB = (ROPE || (NTB_ATTN_QDB && (D == 128 || NTB_ATTN_D64_QB2))) ? 2 : 1;
   static constexpr bool SEAM = NTB_ATTN_SEAM && (D == 128 || ROPE || NTB_ATTN_D64_QB2);
   // (two Q buffers) EARLY_Q: the next unit's Q is requested right after this
   // unit's first K/V tile and each warp releases its staged O rows as soon
@@ -233,12 +225,10 @@ struct Layout {
   // staging is released during the next unit's second tile (D = 128: 6.92-
   // 6.95 vs 7.05-7.33 ms)
   static constexpr bool EARLY_Q = D == 64 || ROPE;
-  static constexpr int NS = D == 128 ? (STAGE_SMEM ? 4 : (QB == 2 ? 3 : 5)) : 8;  // K/V ring entries
+  static constexpr int NS = D == 128 ? (QB == 2 ? 3 : 5) : 8;  // K/V ring entries
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = QB * 2 * Q_BYTES;
-  static constexpr int OFF_STAGE = OFF_KV + NS * SLOT;
-  static constexpr int STAGE_BYTES = STAGE_SMEM ? 8 * 32 * 128 : 0;
-  static constexpr int SMEM = OFF_STAGE + STAGE_BYTES + 1024;
+  static constexpr int SMEM = OFF_KV + NS * SLOT + 1024;
   static constexpr uint32_t T_S0 = 0, T_S1 = BN, T_O0 = 2 * BN, T_O1 = 2 * BN + D;
   static_assert(2 * BN + 2 * D <= 512, "TMEM budget");
   // D = 64 leaves 128 TMEM columns: each query tile gets its own P buffer
@@ -320,7 +310,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&q_full[i], 1);
       // the MMA warp's commit after the unit's last S, plus (TMA-store
       // epilogue) the 8 softmax warps once their staged O rows were read
-      mbar_init(&q_empty[i], (p.o_tma && !L::STAGE_SMEM) ? 9 : 1);
+      mbar_init(&q_empty[i], p.o_tma ? 9 : 1);
       mbar_init(&q_rot[i], 2);                  // rope warps 2-3
     }
     for (int i = 0; i < L::NS; ++i) {
@@ -784,21 +774,12 @@ __global__ void __launch_bounds__(384, 1)
         // (rows past S_q clipped); the producer reloads the buffer only
         // after every warp's TMA has read its staging (q_empty)
         const int qbuf = it % L::QB;
-        uint8_t* stage = L::STAGE_SMEM
-                             ? smem + L::OFF_STAGE + (g * 4 + quad) * (32 * 128)
-                             : smem + L::OFF_Q + qbuf * 2 * L::Q_BYTES +
-                                   ((g * 4 + quad) * L::DCH) * (32 * 128);
+        uint8_t* stage = smem + L::OFF_Q + qbuf * 2 * L::Q_BYTES +
+                         ((g * 4 + quad) * L::DCH) * (32 * 128);
         const int row0 = qt * 2 * BM + tile * BM + quad * 32;
 #pragma unroll
         for (int ch = 0; ch < L::DCH; ++ch) {
-          uint8_t* box = L::STAGE_SMEM ? stage : stage + ch * (32 * 128);
-          if (L::STAGE_SMEM) {
-            // one 4 KB box per warp: the previous box (of this or the last
-            // unit) must have been read by its TMA store
-            if (lane == 0) bulk_wait_read<0>();
-            __syncwarp();
-          }
-          const uint32_t base = smem_u32(box) + lane * 128;
+          const uint32_t base = smem_u32(stage + ch * (32 * 128)) + lane * 128;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             uint32_t w[4];
@@ -810,32 +791,22 @@ __global__ void __launch_bounds__(384, 1)
                          "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
                          : "memory");
           }
-          if (L::STAGE_SMEM) {
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_4d(&maps.o, box, ch * 64, row0, h, b);
-              bulk_commit();
-            }
-          }
         }
-        if (!L::STAGE_SMEM) {
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
 #pragma unroll
-            for (int ch = 0; ch < L::DCH; ++ch)
-              tma_store_4d(&maps.o, stage + ch * (32 * 128), ch * 64, row0, h, b);
-            bulk_commit();
-            if (L::EARLY_Q) {
-              // the Q buffer goes back to the producer once the TMA has read
-              // the staged rows (a few hundred cycles)
-              bulk_wait_read<0>();
-              mbar_arrive(&q_empty[qbuf]);
-            }
+          for (int ch = 0; ch < L::DCH; ++ch)
+            tma_store_4d(&maps.o, stage + ch * (32 * 128), ch * 64, row0, h, b);
+          bulk_commit();
+          if (L::EARLY_Q) {
+            // the Q buffer goes back to the producer once the TMA has read
+            // the staged rows (a few hundred cycles)
+            bulk_wait_read<0>();
+            mbar_arrive(&q_empty[qbuf]);
           }
-          if (!L::EARLY_Q) stage_pending = qbuf;   // released during the next unit (below)
         }
+        if (!L::EARLY_Q) stage_pending = qbuf;   // released during the next unit (below)
         ITR(g, it, 3)
       } else if (qrow < p.Sq) {
         char* obase = reinterpret_cast<char*>(p.o) +
@@ -899,7 +870,7 @@ int launch_attn(const AttnMaps& maps, AttnParams p, cudaStream_t s) {
   cudaError_t e = smem_attr_once(k, L::SMEM, attr);
   if (e != cudaSuccess) return cuda_fail(e, "attention smem attribute");
   // the TMA-store epilogue stages in a second Q buffer or its own area
-  if (L::QB != 2 && !L::STAGE_SMEM) p.o_tma = 0;
+  if (L::QB != 2) p.o_tma = 0;
   // Tail split: when the last round of items would leave more than half of
   // the CTAs idle, its items run as two single-tile units each on twice as
   // many CTAs (a single-tile unit takes ~half to ~3/4 of an item: the chain
