@@ -142,6 +142,13 @@ static int fill_attn(const LaunchArgs& A, int qi, int ki, int vi, int oi, AttnDe
   return NTB_OK;
 }
 
+// read per call (tests vary it): NTB_ROPE_WS_MB, default 512
+static int64_t rope_ws_cap() {
+  const char* e = getenv("NTB_ROPE_WS_MB");
+  const long long mb = e ? atoll(e) : 512;
+  return (int64_t)(mb > 0 ? mb : 1) << 20;
+}
+
 // sdpa(rope(q), rope(k), v): params q, k, v, sin_q, cos_q, sin_k, cos_k, o
 // (catalog.spec_sdpa_rope).  Q is rotated inside the attention kernel (in
 // shared memory between its TMA load and the first MMA, once per query
@@ -174,7 +181,16 @@ int launch_sdpa_rope(const LaunchArgs& A) {
       A.strides[cb + 1] != 1 || !aligned16(A.ptrs[5]) || !aligned16(A.ptrs[6]) ||
       !aligned16(a.k) || (D != 64 && D != 128))
     return fail(NTB_ERR_UNSUPPORTED, layout_msg);
-  void* krot = workspace((size_t)(B * H * S * D) * 2, A.stream);
+  // The rotated K lives in workspace one batch chunk at a time (at most
+  // rope_ws_cap() bytes, default 512 MB): the pre-pass and the attention
+  // alternate per chunk, so the workspace is bounded, not O(B H S D).
+  const int64_t per_batch = H * S * D * 2;
+  int64_t bc = rope_ws_cap() / per_batch;
+  if (bc < 1) bc = 1;
+  if (bc > B) bc = B;
+  const int64_t n_chunks = (B + bc - 1) / bc;
+  bc = (B + n_chunks - 1) / n_chunks;
+  void* krot = workspace((size_t)(bc * per_batch), A.stream);
   if (!krot) return fail(NTB_ERR_CUDA, "sdpa_rope: workspace allocation failed");
   RopeTables rt;
   rt.sin_q = A.ptrs[3];
@@ -192,10 +208,20 @@ int launch_sdpa_rope(const LaunchArgs& A) {
   rc = attn_sm100(ak, A.dtype, A.stream, &rt, /*dry_run=*/true);
   if (rc == NTB_ERR_UNSUPPORTED) return fail(NTB_ERR_UNSUPPORTED, layout_msg);
   if (rc) return rc;
-  rc = rope_rows_vec(a.k, A.ptrs[5], A.ptrs[6], krot, B * H * S, S, pos_div, (int)(D / 2),
-                     A.dtype, A.stream);
-  if (rc) return rc;
-  return attn_sm100(ak, A.dtype, A.stream, &rt);
+  for (int64_t b0 = 0; b0 < B; b0 += bc) {
+    const int64_t nb = B - b0 < bc ? B - b0 : bc;
+    AttnDesc ac = ak;
+    ac.B = nb;
+    ac.q = static_cast<const uint16_t*>(a.q) + b0 * a.qs[0];
+    ac.v = static_cast<const uint16_t*>(a.v) + b0 * a.vs[0];
+    ac.o = static_cast<uint16_t*>(a.o) + b0 * a.os[0];
+    rc = rope_rows_vec(static_cast<const uint16_t*>(a.k) + b0 * ks[0], A.ptrs[5], A.ptrs[6], krot,
+                       nb * H * S, S, pos_div, (int)(D / 2), A.dtype, A.stream);
+    if (rc) return rc;
+    rc = attn_sm100(ac, A.dtype, A.stream, &rt);
+    if (rc) return rc;
+  }
+  return NTB_OK;
 }
 
 int launch_sdpa(const LaunchArgs& A) {

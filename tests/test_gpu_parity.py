@@ -451,6 +451,30 @@ def test_sdpa_rope_fused(dtype, bshd):
     assert (o.float() - o2.float()).abs().max().item() <= 2e-3
 
 
+@pytest.mark.parametrize("bshd", [(3, 1024, 4, 128), (5, 1024, 8, 64)])  # 1 MB per batch
+def test_sdpa_rope_chunked_workspace(bshd, monkeypatch):
+    """The rotated K lives in workspace one batch chunk at a time
+    (NTB_ROPE_WS_MB cap): a 1 MB cap forces one batch per chunk, and the
+    output must be byte-identical to the single-chunk run (the chunking only
+    changes which launch a (b, h) unit lands in)."""
+    b, s, h, d = bshd
+    g = torch.Generator(device=DEV).manual_seed(b * s + d)
+    base = [(torch.rand((b, s, h, d), generator=g, device=DEV) * 2 - 1).half() for _ in range(3)]
+    ang = torch.rand((s, d // 2), generator=g, device=DEV) * 6 - 3
+    sn, cs = torch.sin(ang).half(), torch.cos(ang).half()
+    q, k, v = (t.transpose(1, 2) for t in base)
+    outs = []
+    for cap, launches in (("4096", 1), ("1", b)):
+        monkeypatch.setenv("NTB_ROPE_WS_MB", cap)
+        o = torch.full((b, h, s, d), float("nan"), device=DEV, dtype=torch.float16)
+        with _Paths() as pc:
+            backend.sdpa_rope_launch(q, k, v, sn, cs, sn, cs, o, 128, 128)
+            torch.cuda.synchronize()
+        assert pc.delta["attn_tc"] == launches
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1])
+
+
 def _attn_fp32(q, k, v):
     """Exact attention in fp32 on the GPU, one batch at a time (no TF32):
     the all-heads check at the BASELINE shape."""
