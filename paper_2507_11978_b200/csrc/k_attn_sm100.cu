@@ -60,6 +60,15 @@ static_assert(PCH == 2 || PCH == 4, "P chunks");
 #define NTB_ATTN_PBUF 1  // D = 64: P in its own TMEM columns, S_{j+1} issued during softmax_j
 #endif
 
+#ifndef NTB_ATTN_REG_LO
+#define NTB_ATTN_REG_LO 72   // producer / MMA (/ rope) warps
+#endif
+#ifndef NTB_ATTN_REG_HI
+#define NTB_ATTN_REG_HI 216  // softmax warpgroups (72/216: no spills; 96/200 spilled, 2-4% slower)
+#endif
+// setmaxnreg.inc blocks until the CTA's pool (168 registers x 384 threads at
+// launch) can serve it: a larger split deadlocks
+static_assert(NTB_ATTN_REG_LO * 128 + NTB_ATTN_REG_HI * 256 <= 168 * 384, "register split");
 #ifndef NTB_ATTN_TRACE
 #define NTB_ATTN_TRACE 0  // debug builds: per-phase clock64 stamps of CTA 0's first item
 #endif
@@ -337,7 +346,7 @@ __global__ void __launch_bounds__(384, 1)
   // registers: the producer / MMA warpgroup gives its share to the softmax
   // warpgroups (one 128-column S row per thread lives in registers)
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(NTB_ATTN_REG_LO));
   if (warp == 0) {
     if (elect_one()) {
       tma_prefetch(&maps.q);
@@ -611,7 +620,7 @@ __global__ void __launch_bounds__(384, 1)
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(NTB_ATTN_REG_HI));
     const int g = (warp - 4) >> 2;          // query tile of this warpgroup
     const int quad = warp & 3;              // TMEM lane quadrant
     const int row = quad * 32 + lane;
