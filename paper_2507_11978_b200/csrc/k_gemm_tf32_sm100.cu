@@ -47,6 +47,22 @@ constexpr int T_STAGES = 3;
 constexpr int T_STAGE_C = 8 * 32 * 128;              // 8 epilogue warps x (32 rows x 32 fp32)
 constexpr int T_SMEM = T_STAGES * T_STAGE + T_STAGE_C + 1024;
 constexpr int T_THREADS = 384;
+#ifndef NTB_TF32_REGSPLIT
+#define NTB_TF32_REGSPLIT 1  // 0: no setmaxnreg (A/B: the epilogue then spills; ~2% slower)
+#endif
+// registers to the epilogue warps (128 fp32 partial sums per thread):
+// 72 x 128 + 216 x 256 = the launch pool of 168 x 384
+#if NTB_TF32_REGSPLIT
+#ifndef NTB_TF32_REG_LO
+#define NTB_TF32_REG_LO 72
+#endif
+#define NTB_TF32_REG_HI ((168 * 384 - NTB_TF32_REG_LO * 128) / 256 / 8 * 8)
+#define TF32_REG_DEC asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(NTB_TF32_REG_LO));
+#define TF32_REG_INC asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(NTB_TF32_REG_HI));
+#else
+#define TF32_REG_DEC
+#define TF32_REG_INC
+#endif
 #ifndef NTB_TF32_CHUNK
 #define NTB_TF32_CHUNK 4   // K blocks (x 32) accumulated in TMEM before the epilogue drains them
 #endif
@@ -192,6 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
   pdl_trigger();
 
   if (warp == 0) {
+    TF32_REG_DEC
     if (elect_one()) {
       int st = 0;
       uint32_t ph = 0;
@@ -241,6 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
       }
     }
   } else if (warp == 1 && rank == 1) {
+    TF32_REG_DEC
     // CTA 1's publisher: after its 2 converter warps (named barrier 1 + stage),
     // one cluster-scope release-arrive on CTA 0's "stage ready" barrier (the
     // release costs ~1k cycles, kept off the converters' path)
@@ -252,6 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
         if (++st == T_STAGES) st = 0;
       }
   } else if (warp == 1) {
+    TF32_REG_DEC
     if (elect_one()) {
       // K chunks of T_CHUNK blocks alternate between the two TMEM buffers,
       // each starting from zero; the epilogue adds them in fp32 registers
@@ -295,6 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
       }
     }
   } else if (warp == 2 || warp == 3) {
+    TF32_REG_DEC
     // lo converters: 2 x 16 KB of raw tiles -> 2 x 16 KB of lo tiles per stage
     const int ct = threadIdx.x - 64;
     int st = 0;
@@ -338,6 +358,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(T_THREADS, 1)
         }
       }
   } else if (warp >= 4) {
+    TF32_REG_INC
     // 8 epilogue warps: TMEM lane quadrant = warp % 4, column half = (warp - 4) / 4.
     // Each thread keeps its row's 128 columns as fp32 partial sums across the
     // K chunks (the tensor core's own accumulation is not round-to-nearest:
