@@ -53,8 +53,11 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef NTB_ATTN_PCH
 #define NTB_ATTN_PCH 4  // P_j released to the MMA warp in this many key chunks (4: ~2% over 2)
 #endif
-constexpr int PCH = NTB_ATTN_PCH;
-static_assert(PCH == 2 || PCH == 4, "P chunks");
+#ifndef NTB_ATTN_PCH64
+#define NTB_ATTN_PCH64 2  // the same at D = 64 (2: 78.1-78.3 vs 79.2-79.5 us at the paper shape)
+#endif
+static_assert((NTB_ATTN_PCH == 2 || NTB_ATTN_PCH == 4) && (NTB_ATTN_PCH64 == 2 || NTB_ATTN_PCH64 == 4),
+              "P chunks");
 
 #ifndef NTB_ATTN_PBUF
 #define NTB_ATTN_PBUF 1  // D = 64: P in its own TMEM columns, S_{j+1} issued during softmax_j
@@ -215,6 +218,7 @@ __device__ __forceinline__ void rope_tile(uint8_t* tile, int chunk_bytes, int ro
 template <int D, bool ROPE = false>
 struct Layout {
   static constexpr int DCH = D / 64;               // 128B chunks along D
+  static constexpr int PCH = D == 64 ? NTB_ATTN_PCH64 : NTB_ATTN_PCH;
   static constexpr int Q_BYTES = BM * D * 2;       // one query tile
   static constexpr int CH = BN * 128;              // one 64-wide chunk of a K/V tile
   static constexpr int SLOT = DCH * CH;            // one K or V tile
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t q_full[L::QB], q_empty[L::QB], kv_full[L::NS], kv_empty[L::NS],
-      s_full[2], p_full[2][PCH], o_full[2], o_empty[2], q_rot[L::QB], s_free[2], pv_done[2];
+      s_full[2], p_full[2][L::PCH], o_full[2], o_empty[2], q_rot[L::QB], s_free[2], pv_done[2];
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&s_full[g], 1);
-      for (int q = 0; q < PCH; ++q) mbar_init(&p_full[g][q], 4);
+      for (int q = 0; q < L::PCH; ++q) mbar_init(&p_full[g][q], 4);
       mbar_init(&o_full[g], 1);
       mbar_init(&o_empty[g], 4);
       mbar_init(&s_free[g], 4);    // SEP_P: S columns read by the 4 softmax warps
@@ -456,12 +460,12 @@ __global__ void __launch_bounds__(384, 1)
         }
         mma_commit(&s_full[g]);
       };
-      // P.V for one chunk of the keys (P is released by the softmax in PCH chunks)
+      // P.V for one chunk of the keys (P is released by the softmax in L::PCH chunks)
       auto issue_pv = [&](int g, uint32_t vseq, bool first, int half) {
         const uint32_t v_addr = slot_addr(vseq);
 #pragma unroll
-        for (int k2 = 0; k2 < BN / 16 / PCH; ++k2) {
-          const int kk = half * (BN / 16 / PCH) + k2;
+        for (int k2 = 0; k2 < BN / 16 / L::PCH; ++k2) {
+          const int kk = half * (BN / 16 / L::PCH) + k2;
           mma_f16_ts(tmem + (g ? L::T_O1 : L::T_O0), tmem + (g ? L::T_P1 : L::T_P0) + kk * 8,
                      umma_desc_sw128(v_addr + kk * 2048, L::CH, 1024), idesc_o,
                      !(first && kk == 0));
@@ -543,7 +547,7 @@ __global__ void __launch_bounds__(384, 1)
           wait_kv(vseq);
           issue_pv(0, vseq, j == 0, 0);
 #pragma unroll
-          for (int q = 1; q < PCH; ++q) {
+          for (int q = 1; q < L::PCH; ++q) {
             mbar_wait(&p_full[0][q], t & 1);
             tc_fence_after();
             issue_pv(0, vseq, j == 0, q);
@@ -578,7 +582,7 @@ __global__ void __launch_bounds__(384, 1)
           }
           issue_pv(1, vseq, j == 0, 0);
 #pragma unroll
-          for (int q = 1; q < PCH; ++q) {
+          for (int q = 1; q < L::PCH; ++q) {
             mbar_wait(&p_full[1][q], t & 1);
             tc_fence_after();
             issue_pv(1, vseq, j == 0, q);
@@ -708,10 +712,10 @@ __global__ void __launch_bounds__(384, 1)
           tc_fence_after();
         }
 #pragma unroll
-        for (int half = 0; half < PCH; ++half) {
+        for (int half = 0; half < L::PCH; ++half) {
 #pragma unroll
-          for (int c2 = 0; c2 < BN / 32 / PCH; ++c2) {
-            const int ch = half * (BN / 32 / PCH) + c2;
+          for (int c2 = 0; c2 < BN / 32 / L::PCH; ++c2) {
+            const int ch = half * (BN / 32 / L::PCH) + c2;
             uint32_t pk[16];
             // staged: all 16 scale/subtract FFMA2, then all 2^x, then the
             // sums and packs - independent work laid out for the scheduler
@@ -739,9 +743,9 @@ __global__ void __launch_bounds__(384, 1)
             tmem_st_32x32b_x16(t_p + ch * 16, pk);
           }
           // release this chunk of P_j to the MMA warp
-          if (half == PCH - 1) { TRACE_SM(g, j, 6) }
+          if (half == L::PCH - 1) { TRACE_SM(g, j, 6) }
           tmem_st_wait();
-          if (half == PCH - 1) { TRACE_SM(g, j, 7) }
+          if (half == L::PCH - 1) { TRACE_SM(g, j, 7) }
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&p_full[g][half]);

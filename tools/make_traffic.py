@@ -36,6 +36,16 @@ FAMILY = {"softmax": "row_stream", "rms_norm": "row_stream", "add_2^20": "ew_vec
           "bmm": "gemm_pair", "mm_f32": "gemm_tf32", "bmm_f32": "gemm_tf32",
           "conv2d": "conv_fused", "conv2d_f32": "gemm_tf32", "sdpa": "attn_fwd", "rope": "rope_vec",
           "sdpa_rope": "attn_fwd"}
+def traffic(d):
+    # bytes written = between the DRAM write counter and that plus one L2 of
+    # dirty lines still resident at kernel end; the SM-sourced L2 write
+    # sectors (32 B each) estimate it, capped by that bound (partial-sector
+    # stores count a sector per store)
+    dw = d.get("dram__bytes_write.sum", 0)
+    wr = max(dw, min(32 * d.get("lts__t_sectors_srcunit_tex_op_write.sum", 0), dw + L2_BYTES))
+    return d.get("dram__bytes_read.sum", 0) + wr
+
+
 ids = sorted(data)
 out, seen = {}, defaultdict(int)
 k = 0
@@ -45,14 +55,20 @@ for key in order:
         k += 1
     if k == len(ids):
         break
-    d = data[ids[k]]
-    # bytes written = between the DRAM write counter and that plus one L2 of
-    # dirty lines still resident at kernel end; the SM-sourced L2 write
-    # sectors (32 B each) estimate it, capped by that bound (partial-sector
-    # stores count a sector per store)
-    dw = d.get("dram__bytes_write.sum", 0)
-    wr = max(dw, min(32 * d.get("lts__t_sectors_srcunit_tex_op_write.sum", 0), dw + L2_BYTES))
-    out[key] = int(d.get("dram__bytes_read.sum", 0) + wr)
+    # sdpa_rope runs one attention launch per batch chunk (each after its
+    # rope_vec K pre-pass): the key's traffic is the sum of those launches
+    group = [ids[k]]
+    if key == "sdpa_rope":
+        j = k + 1
+        while j < len(ids) and ("attn_fwd" in names[ids[j]] or "rope_vec" in names[ids[j]]):
+            if "attn_fwd" in names[ids[j]]:
+                group.append(ids[j])
+            j += 1
+        k = j - 1
+    tot = 0
+    for lid in group:
+        tot += traffic(data[lid])
+    out[key] = int(tot)
     k += 1
 out["_note"] = ("per launch, ncu on tools/traffic_probe.py (cold L2 per replay): "
                 "dram__bytes_read.sum + writes "
@@ -60,7 +76,8 @@ out["_note"] = ("per launch, ncu on tools/traffic_probe.py (cold L2 per replay):
                 "126 MB)), W = dram__bytes_write.sum: writes left dirty in the L2 at kernel end "
                 "never reach DRAM inside the capture (the L2 write sectors count them), but at "
                 "most one L2 of them can (partial-sector stores, e.g. the attention epilogue's "
-                "16 B per row, count one sector per store). sdpa_rope: the attention kernel "
-                "only (its K pre-pass is a separate rope_vec launch).")
+                "16 B per row, count one sector per store). sdpa_rope: its attention launches "
+                "summed, one per batch chunk of the rotated-K workspace (the K pre-pass is a "
+                "separate rope_vec launch per chunk).")
 json.dump(out, open("profiles/traffic.json", "w"), indent=1)
 print(json.dumps(out, indent=1))
