@@ -72,6 +72,9 @@ static_assert((NTB_ATTN_PCH == 2 || NTB_ATTN_PCH == 4) && (NTB_ATTN_PCH64 == 2 |
 // setmaxnreg.inc blocks until the CTA's pool (168 registers x 384 threads at
 // launch) can serve it: a larger split deadlocks
 static_assert(NTB_ATTN_REG_LO * 128 + NTB_ATTN_REG_HI * 256 <= 168 * 384, "register split");
+#ifndef NTB_ATTN_PDL
+#define NTB_ATTN_PDL 1  // programmatic dependent launch (prologue under the previous kernel's tail)
+#endif
 #ifndef NTB_ATTN_TRACE
 #define NTB_ATTN_TRACE 0  // debug builds: per-phase clock64 stamps of CTA 0's first item
 #endif
@@ -347,6 +350,12 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+#if NTB_ATTN_PDL
+  // launched with programmatic stream serialization: the set-up above
+  // overlaps the previous kernel's tail; nothing global is read before this
+  pdl_wait();
+  pdl_trigger();
+#endif
   // registers: the producer / MMA warpgroup gives its share to the softmax
   // warpgroups (one 128-column S row per thread lives in registers)
   if (warp < 4) {
@@ -908,7 +917,8 @@ int launch_attn(const AttnMaps& maps, AttnParams p, cudaStream_t s) {
       }
     }
   }
-  k<<<grid, 384, L::SMEM, s>>>(maps, p);
+  if (NTB_ATTN_PDL) launch_pdl(k, dim3(grid), dim3(384), L::SMEM, s, maps, p);
+  else k<<<grid, 384, L::SMEM, s>>>(maps, p);
 #if NTB_ATTN_TRACE
   {
     static long long h[2 * 64 * 8 + 64 * 8];

@@ -828,7 +828,12 @@ def test_pdl_dependent_chains():
     m0 = (torch.rand((512, 512), device=DEV) * 2 - 1).to(f16)
     e = (torch.eye(512, device=DEV) * 0.5).to(f16)
     mats = [m0] + [torch.empty_like(m0) for _ in range(3)]
-    outs = bufs[1:] + rows[1:] + mats[1:]
+    # attention: each output is the next launch's query (the persistent
+    # attention kernel is PDL-launched too)
+    qa = [(torch.rand((1, 2, 640, 128), device=DEV) * 2 - 1).to(f16)]
+    qa += [torch.empty_like(qa[0]) for _ in range(3)]
+    ka, va = ((torch.rand((1, 2, 640, 128), device=DEV) * 2 - 1).to(f16) for _ in range(2))
+    outs = bufs[1:] + rows[1:] + mats[1:] + qa[1:]
 
     def run(sync):
         def s():
@@ -845,6 +850,9 @@ def test_pdl_dependent_chains():
             s()
         for i in range(3):
             backend.mm_launch(mats[i], e, mats[i + 1], 128, 128, 64)
+            s()
+        for i in range(3):
+            backend.sdpa_launch(qa[i], ka, va, qa[i + 1], 128, 128)
             s()
 
     def nan_fill():
