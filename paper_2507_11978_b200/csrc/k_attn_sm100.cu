@@ -714,9 +714,11 @@ __global__ void __launch_bounds__(384, 1)
         TRACE_SM(g, j, 3)
         const float2 nm2 = make_float2(-m_new, -m_new);
         float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        if (L::SEP_P && j > 0) {
-          // the P buffer is free once the previous tile's P.V completed
-          // (j = 0: the previous item's last P.V completed before o_full)
+        if (L::SEP_P && t > 0) {
+          // the P buffer is free once the previous tile's P.V completed (at
+          // j = 0 that is the previous unit's last P.V, complete before
+          // o_full: the wait returns at once, but every pv_done phase is
+          // consumed before the next commit - compute-sanitizer synccheck)
           mbar_wait(&pv_done[g], (t - 1) & 1);
           tc_fence_after();
         }

@@ -30,8 +30,28 @@ elif kind == "sdpa":
     o = torch.zeros_like(q)
     B.sdpa_launch(q, kk, v, o, 128, 128)
     torch.cuda.synchronize()
-    ref = torch.nn.functional.scaled_dot_product_attention(q.float(), kk.float(), v.float())
+    # math reference (cuBLAS GEMMs): PyTorch's own SDPA kernels would be in
+    # the sanitizer's report too
+    ref = torch.softmax(q.float() @ kk.float().transpose(-1, -2) / d ** 0.5, -1) @ v.float()
     print("sdpa max err", (o.float() - ref).abs().max().item(), B.path_counts())
+elif kind == "sdpa_rope":
+    b, s_, h, d = (int(x) for x in sys.argv[2:6])
+    base = [T((b, s_, h, d)) for _ in range(3)]
+    ang = torch.rand((s_, d // 2), device=dev) * 6 - 3
+    sn, cs = torch.sin(ang).half(), torch.cos(ang).half()
+    q, kk, v = (x.transpose(1, 2) for x in base)
+    o = torch.zeros((b, h, s_, d), device=dev, dtype=torch.float16)
+    B.sdpa_rope_launch(q, kk, v, sn, cs, sn, cs, o, 128, 128)
+    torch.cuda.synchronize()
+
+    def rot(x):
+        x = x.float()
+        x0, x1 = x[..., :d // 2], x[..., d // 2:]
+        c, s = cs.float(), sn.float()
+        return torch.cat([x0 * c - x1 * s, x0 * s + x1 * c], -1).half().float()
+
+    ref = torch.softmax(rot(q) @ rot(kk).transpose(-1, -2) / d ** 0.5, -1) @ v.float()
+    print("sdpa_rope max err", (o.float() - ref).abs().max().item(), B.path_counts())
 elif kind == "mm":
     m, n, k = (int(x) for x in sys.argv[2:5])
     a, b = T((m, k)), T((k, n))
@@ -39,6 +59,16 @@ elif kind == "mm":
     B.mm_launch(a, b, c, 128, 128, 64)
     torch.cuda.synchronize()
     print("mm", m, n, k, "max err", (c.float() - a.float() @ b.float()).abs().max().item(),
+          {k_: v for k_, v in B.path_counts().items() if v})
+elif kind == "mm32":   # fp32 operands: the 3xTF32 tcgen05 kernel
+    m, n, k = (int(x) for x in sys.argv[2:5])
+    a = torch.rand((m, k), device=dev) * 2 - 1
+    b = torch.rand((k, n), device=dev) * 2 - 1
+    c = torch.zeros((m, n), device=dev)
+    B.mm_launch(a, b, c, 128, 128, 64)
+    torch.cuda.synchronize()
+    ref = (a.double() @ b.double()).float()
+    print("mm32", m, n, k, "max err", (c - ref).abs().max().item(),
           {k_: v for k_, v in B.path_counts().items() if v})
 elif kind == "bmm":
     bt, m, n, k = (int(x) for x in sys.argv[2:6])
